@@ -1,0 +1,193 @@
+"""Generate golden vectors by running the REFERENCE implementation itself.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports the unmodified reference (``sparseops`` from
+/root/reference/pkg/src), feeds it the fixture matrices of oracle/fixtures.py and
+records its outputs bit for bit in small ``.npz`` files next to this script.
+The GPU box never reads /root/reference: tests there use these committed files.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REPO)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import sparseops as sp  # noqa: E402  (the reference)
+
+from oracle import fixtures  # noqa: E402
+
+REF = sp.create_device("reference")
+PREC = {np.float64: sp.Precision.double, np.float32: sp.Precision.single}
+WIDTH = {np.int32: sp.IndexWidth.i32, np.int64: sp.IndexWidth.i64}
+
+
+def ref_csr(rows, cols, ri, ci, v, vdt=np.float64, idt=np.int32):
+    coo = sp.coo_from_arrays(REF, rows, cols, ri, ci, v, PREC[vdt], WIDTH[idt])
+    return sp.csr_from_coo(coo)
+
+
+def vec(a, dt):
+    return sp.dense_from_array(REF, np.asarray(a, dtype=dt).copy())
+
+
+def pack(mats):
+    """Concatenate a list of dicts of arrays with offsets (one npz instead of hundreds)."""
+    out = {}
+    keys = mats[0].keys()
+    for k in keys:
+        arrs = [np.atleast_1d(m[k]) for m in mats]
+        out[k] = np.concatenate(arrs) if arrs else np.zeros(0)
+        out[k + "_off"] = np.concatenate([[0], np.cumsum([a.size for a in arrs])]).astype(np.int64)
+    return out
+
+
+def spmv_suite():
+    """First 60 matrices of the acceptance oracle suite (seed 2024), every
+    value/index instantiation: CSR and COO SpMV outputs of the reference."""
+    suite = fixtures.oracle_suite(60, 2024)
+    for vdt in (np.float64, np.float32):
+        for idt in (np.int32, np.int64):
+            mats = []
+            for rows, cols, ri, ci, v, bv in suite:
+                a = ref_csr(rows, cols, ri, ci, v, vdt, idt)
+                b = vec(bv, vdt)
+                x = sp.dense_create(REF, rows, 1, PREC[vdt], np.nan)
+                sp.spmv_csr(a, b, x)
+                y = sp.dense_create(REF, rows, 1, PREC[vdt], np.nan)
+                sp.spmv_coo(sp.coo_from_csr(a), b, y)
+                assert np.array_equal(x.values, y.values)
+                mats.append(dict(shape=np.array([rows, cols], np.int64), row_ptrs=a.row_ptrs,
+                                 col_idxs=a.col_idxs, values=a.values, b=b.values, x=x.values))
+            name = f"spmv_suite_{np.dtype(vdt).name}_{np.dtype(idt).name}.npz"
+            np.savez_compressed(os.path.join(HERE, name), **pack(mats))
+
+
+def canonicalization():
+    """coo_from_arrays on raw triplets with duplicates, out of order, explicit zeros."""
+    rng = np.random.default_rng(11)
+    cases = []
+    for rows, cols, m in ((7, 5, 40), (50, 60, 900), (1, 1, 5), (300, 3, 2000)):
+        ri = rng.integers(0, rows, m)
+        ci = rng.integers(0, cols, m)
+        v = rng.standard_normal(m)
+        v[rng.random(m) < 0.1] = 0.0
+        cases.append((rows, cols, ri, ci, v))
+    mats = []
+    for vdt in (np.float64, np.float32):
+        for rows, cols, ri, ci, v in cases:
+            coo = sp.coo_from_arrays(REF, rows, cols, ri, ci, v, PREC[vdt], sp.IndexWidth.i64)
+            csr = sp.csr_from_coo(coo)
+            mats.append(dict(meta=np.array([rows, cols, 0 if vdt == np.float64 else 1], np.int64),
+                             ri=ri.astype(np.int64), ci=ci.astype(np.int64), v=v,
+                             out_r=coo.row_idxs, out_c=coo.col_idxs,
+                             out_v=coo.values.astype(np.float64), row_ptrs=csr.row_ptrs))
+    np.savez_compressed(os.path.join(HERE, "canonicalize.npz"), **pack(mats))
+
+
+def stencils_and_jacobi():
+    out = {}
+    for name, (p, dim, c) in {"poisson2d_32": (32, 2, 0.0), "poisson3d_12": (12, 3, 0.0),
+                              "convdiff3d_12": (12, 3, 0.5)}.items():
+        if dim == 2:
+            n, ri, ci, v = fixtures.poisson2d_triplets(p)
+        else:
+            n, ri, ci, v = fixtures.stencil3d_triplets(p, c)
+        a = ref_csr(n, n, ri, ci, v)
+        bv = np.random.default_rng(0).random(n)
+        x = sp.dense_create(REF, n, 1, sp.Precision.double, 0.0)
+        sp.spmv_csr(a, vec(bv, np.float64), x)
+        jac = sp.jacobi_create(a)
+        out[f"{name}_row_ptrs"] = a.row_ptrs
+        out[f"{name}_col_idxs"] = a.col_idxs
+        out[f"{name}_values"] = a.values
+        out[f"{name}_b"] = bv
+        out[f"{name}_x"] = x.values
+        out[f"{name}_inv_diag"] = jac.inv_diag
+    np.savez_compressed(os.path.join(HERE, "stencils.npz"), **out)
+
+
+def solver_goldens():
+    """Reference solver runs: iteration counts, residual histories and final x."""
+    out, meta = {}, {}
+    runs = [
+        # name, generator args, solver class, precision, criteria, krylov_dim
+        ("cg_jacobi_poisson3d_16", (16, 0.0), "Cg", np.float64, 100000, 1e-8, None),
+        ("cg_jacobi_poisson3d_16_f32", (16, 0.0), "Cg", np.float32, 100000, 1e-5, None),
+        ("gmres30_jacobi_convdiff3d_16", (16, 0.5), "Gmres", np.float64, 5000, 1e-8, 30),
+        ("cgs_jacobi_convdiff3d_16", (16, 0.5), "Cgs", np.float64, 5000, 1e-8, None),
+        ("cg_fixed25_poisson3d_12", (12, 0.0), "Cg", np.float64, 25, None, None),
+        ("gmres5_fixed45_poisson3d_12", (12, 0.0), "Gmres", np.float64, 45, None, 5),
+        ("gmres10_jacobi_convdiff3d_12", (12, 0.5), "Gmres", np.float64, 5000, 1e-9, 10),
+        ("cg_jacobi_poisson3d_32", (32, 0.0), "Cg", np.float64, 100000, 1e-8, None),
+        ("gmres30_jacobi_convdiff3d_32", (32, 0.5), "Gmres", np.float64, 5000, 1e-8, 30),
+    ]
+    for name, (p, c), cls, vdt, max_iters, rf, dim in runs:
+        n, ri, ci, v = fixtures.stencil3d_triplets(p, c)
+        a = ref_csr(n, n, ri, ci, v, vdt)
+        crit = [sp.Iteration(max_iters)] + ([sp.ResidualNorm(rf)] if rf else [])
+        m = sp.jacobi_create(a)
+        b = sp.dense_create(REF, n, 1, PREC[vdt], 1.0)
+        x = sp.dense_create(REF, n, 1, PREC[vdt], 0.0)
+        kw = {"krylov_dim": dim} if cls == "Gmres" else {}
+        log = getattr(sp, cls)(a, criteria=crit, preconditioner=m, **kw).solve(b, x)
+        meta[name] = dict(p=p, c=c, solver=cls.lower(), dtype=np.dtype(vdt).name,
+                          max_iters=max_iters, reduction_factor=rf, krylov_dim=dim,
+                          iterations=log.iterations, converged=log.converged,
+                          stop_reason=log.stop_reason)
+        out[f"{name}_history"] = np.asarray(log.residual_history, np.float64)
+        out[f"{name}_x"] = x.values.copy()
+    np.savez_compressed(os.path.join(HERE, "solvers.npz"), **out)
+    # counts measured with this same reference in the survey container;
+    # too slow to rerun here, recorded as constants.
+    meta["_survey_probe"] = {
+        "cg_jacobi_poisson3d_rtol1e-8": {"16": 39, "32": 79, "64": 159, "96": 239,
+                                         "128": 319, "256": 611},
+        "gmres30_jacobi_convdiff3d_c0.5_rtol1e-8": {"16": 81, "32": 227, "64": 330, "128": 585},
+    }
+    with open(os.path.join(HERE, "solvers.json"), "w") as fh:
+        json.dump(meta, fh, indent=1, sort_keys=True)
+
+
+def blas1():
+    """dot / axpy / scal / norm2 bit patterns (reference device and omp[3])."""
+    rng = np.random.default_rng(5)
+    out = {}
+    for vdt in (np.float64, np.float32):
+        nm = np.dtype(vdt).name
+        xv = rng.standard_normal(20001).astype(vdt)
+        yv = rng.standard_normal(20001).astype(vdt)
+        x, y = vec(xv, vdt), vec(yv, vdt)
+        out[f"{nm}_x"], out[f"{nm}_y"] = xv, yv
+        out[f"{nm}_dot1"] = np.float64(sp.dot(x, y))
+        omp3 = sp.create_device("omp", threads=3)
+        x3 = sp.dense_from_array(omp3, xv.copy())
+        y3 = sp.dense_from_array(omp3, yv.copy())
+        out[f"{nm}_dot3"] = np.float64(sp.dot(x3, y3))
+        out[f"{nm}_norm1"] = np.float64(sp.norm2(x))
+        yy = vec(yv, vdt)
+        sp.axpy(-0.7310585786300049, x, yy)
+        out[f"{nm}_axpy"] = yy.values.copy()
+        xx = vec(xv, vdt)
+        sp.scal(1.0 / 3.0, xx)
+        out[f"{nm}_scal"] = xx.values.copy()
+    np.savez_compressed(os.path.join(HERE, "blas1.npz"), **out)
+
+
+if __name__ == "__main__":
+    spmv_suite()
+    canonicalization()
+    stencils_and_jacobi()
+    blas1()
+    solver_goldens()
+    print("golden fixtures written to", HERE)
