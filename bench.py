@@ -1,0 +1,317 @@
+"""Benchmark: Jacobi-preconditioned CG, fp64, 3-D 7-point Poisson 128^3 (BASELINE config #2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one full solve (b = 1, x0 = 0, rtol 1e-8 -> ~319 iterations) through the
+device solver.  `value` = CG iterations per second over all ranks with every input
+resident in HBM (device-timed with CUDA events, max over ranks); `e2e` = the same
+metric through the public frontend API (pysparseops) with host buffers: each step
+copies b and x0 from pinned host memory, solves, and copies x back.
+
+`roofline` is for the dominant kernel, the CSR SpMV (TMA-staged stream kernel) that
+runs once per CG iteration: algorithmic bytes per launch (12*nnz +
+4*(n+1) + 8n + 8n = 216,924,164 B at 128^3) / its CUDA-event launch duration,
+against the measured HBM copy bandwidth in MEASURED_PEAKS.json.  `cpu_baseline` is
+the oracle port (oracle/sbref.cpp) of the reference's CG on this host's cores for a
+bounded sample of iterations.
+
+Multi-GPU (torchrun, N > 1): each rank runs the same single-GPU solve (replicas;
+the row-partitioned NCCL solver is reported separately by bench_dist.py).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "SpMV GB/s & % HBM roofline; CG solve time/iters/s, Poisson-3D fp64, 1/2/4/8 GPU"
+P = 128
+RTOL = 1e-8
+
+
+def _peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks",
+               0x1: "gpu_idle"}
+
+    def __init__(self, index):
+        self.samples, self.reasons = [], set()
+        self.stop = threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.nv:
+            self.stop.set()
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _max_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def cpu_baseline_sample(iters=60):
+    """Oracle port of the reference's Jacobi-CG (oracle/sbref.cpp) on all host threads,
+    fixed-iteration sample at 128^3 -> iterations/s."""
+    import numpy as np
+
+    from oracle import fixtures, sbref
+
+    rp, ci, v = fixtures.stencil_csr(P, dim=3)
+    inv, _ = sbref.jacobi_create(rp, ci, v)
+    b = np.ones(rp.size - 1)
+    threads = len(os.sched_getaffinity(0))
+    sbref.solve("cg", rp, ci, v, b, inv_diag=inv, max_iters=2, threads=threads)  # warm
+    t0 = time.perf_counter()
+    log, _ = sbref.solve("cg", rp, ci, v, b, inv_diag=inv, max_iters=iters, threads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": log.iterations / dt, "unit": "CG iters/s", "cores": threads, "kind": "port",
+            "sample": f"{log.iterations} fixed Jacobi-CG iterations, fp64 Poisson 128^3, "
+                      f"oracle/sbref.cpp (C++ restatement of the reference), {dt:.2f} s"}
+
+
+def run_reference(args):
+    world, rank, _ = _dist()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        if rank != 0:
+            dist.barrier()
+            return
+    for _ in range(args.warmup):
+        cpu_baseline_sample(10)
+    vals = [cpu_baseline_sample(30)["value"] for _ in range(args.steps)]
+    base = cpu_baseline_sample(30)
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "CG iters/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 30 * 1000.0 / v, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "Jacobi-CG fp64 3-D 7-pt Poisson 128^3, rtol 1e-8 "
+                                   "(fixed-iteration CPU sample of 30 iterations per step)"},
+            "cpu_baseline": {**base, "value": v},
+            "e2e": {"value": v, "unit": "CG iters/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2510_08230_b200 import gen
+    from paper_2510_08230_b200 import pysparseops as pg
+    from paper_2510_08230_b200 import sparseops as sp
+
+    dev = sp.create_device("cuda", local)
+    stream = torch.cuda.current_stream()
+    a = gen.poisson3d(dev, P)
+    n, nnz = a.rows, a.nnz
+    m = sp.jacobi_create(a)
+    solver = sp.Cg(a, criteria=[sp.Iteration(100000), sp.ResidualNorm(RTOL)], preconditioner=m)
+    b = sp.dense_create(dev, n, 1, sp.Precision.double, 1.0)
+    x = sp.dense_create(dev, n, 1, sp.Precision.double, 0.0)
+
+    def step():
+        x.values.zero_()
+        return solver.solve(b, x)
+
+    for _ in range(max(args.warmup, 1)):
+        log = step()
+    torch.cuda.synchronize()
+    _barrier(world)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = 0
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            log = step()
+            iters += log.iterations
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    ms_max = _max_over_ranks(ms, world)
+    _barrier(world)
+    total_iters = iters * world
+    value = total_iters / (ms_max / 1000.0)
+
+    # ---- dominant kernel: the CSR SpMV, timed live with CUDA events on its stream
+    p_vec = sp.dense_create(dev, n, 1, sp.Precision.double, 1.0)
+    q_vec = sp.dense_create(dev, n, 1, sp.Precision.double, 0.0)
+    for _ in range(5):
+        a.apply(p_vec, q_vec)
+    reps = 50
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    s0.record(stream)
+    for _ in range(reps):
+        a.apply(p_vec, q_vec)
+    s1.record(stream)
+    torch.cuda.synchronize()
+    spmv_ms = s0.elapsed_time(s1) / reps
+    spmv_bytes = 12 * nnz + 4 * (n + 1) + 8 * n + 8 * n
+    peak, peak_kind = _peaks()
+    achieved = spmv_bytes / (spmv_ms / 1e3) / 1e9
+    cg_iter_bytes = (12 * nnz + 4 * (n + 1)) + 13 * 8 * n
+    cg_iter_ms = ms / max(iters, 1)
+
+    # ---- e2e: public frontend API with host buffers (pinned), copies inside the region
+    pdev = pg.device("cuda", local)
+    bh = torch.ones(n, dtype=torch.float64).pin_memory()
+    x0h = torch.zeros(n, dtype=torch.float64).pin_memory()
+    xh = torch.empty(n, dtype=torch.float64).pin_memory()
+    cg = pg.solver.cg(pdev, a, pg.preconditioner.Jacobi(pdev, a), max_iters=100000,
+                      reduction_factor=RTOL)
+
+    def e2e_step():
+        bt = pg.as_tensor(bh.to(dev.torch, non_blocking=True), device=pdev)
+        xt = pg.as_tensor(x0h.to(dev.torch, non_blocking=True), device=pdev)
+        logger, res = cg.apply(bt, xt)
+        xh.copy_(res.values, non_blocking=True)
+        return logger
+
+    for _ in range(max(args.warmup, 1)):
+        e2e_step()
+    torch.cuda.synchronize()
+    _barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_iters = 0
+    e0.record(stream)
+    for _ in range(args.steps):
+        e_iters += e2e_step().iterations
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e_ms = _max_over_ranks(e0.elapsed_time(e1), world)
+    e2e_value = e_iters * world / (e_ms / 1e3)
+    assert abs(float(xh[n // 2]) - float(x.values[n // 2])) <= 1e-6 * abs(float(x.values[n // 2]))
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    cpu = cpu_baseline_sample() if not args.no_cpu else None
+    line = {
+        "metric": METRIC, "value": value, "unit": "CG iters/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (device-generated 7-point Poisson stencil, b = 1, x0 = 0)",
+        "config": {"workload": "Jacobi-CG fp64 3-D 7-pt Poisson 128^3 (n=2,097,152, "
+                               "nnz=14,581,760), rtol 1e-8, CSR",
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (CG working set 284 MB vs 126 MB L2); no flush"},
+        "iterations_per_solve": log.iterations,
+        "solve_ms": ms / args.steps,
+        "cg_iteration": {"ms": cg_iter_ms, "alg_bytes": cg_iter_bytes,
+                         "gbs": cg_iter_bytes / (cg_iter_ms / 1e3) / 1e9,
+                         "frac_of_hbm": cg_iter_bytes / (cg_iter_ms / 1e3) / 1e9 / peak},
+        "spmv": {"kernel": a.kernel, "us": spmv_ms * 1e3, "gbs": achieved,
+                 "gflops": 2 * nnz / (spmv_ms / 1e3) / 1e9},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": f"csr_{a.kernel}_kernel<double,int>",
+                     "alg_bytes_per_launch": spmv_bytes, "peak_source": peak_kind},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "CG iters/s", "h2d_bytes_per_step": 2 * 8 * n,
+                "d2h_bytes_per_step": 8 * n + 64},
+        "gpu_launches": args.steps * (2 + 3 * log.iterations),
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

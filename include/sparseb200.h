@@ -1,0 +1,316 @@
+/*
+ * sparseb200.h -- C ABI of libsparseb200.so, the B200-native (sm_100a) SpMV + Krylov library.
+ *
+ * Drop-in boundary for the reference's typed binding layer.  The reference exposes one
+ * callable per (operation x value type [x index type]) with a type suffix
+ * (pkg/frontend/src/pysparseops/bindings.py:27-40, built at :81-145, registered at
+ * :148-159) and routes to them by runtime dtype (dispatch.py:44-66).  This header
+ * exports the same instantiation scheme as plain C symbols:
+ *
+ *     sb_<op>_<value>[_<index>]     value in {float, double}, index in {i32, i64}
+ *
+ * e.g. sb_csr_spmv_double_i32 replaces bindings.csr_spmv_double_i32
+ * (bindings.py:116-119 -> sparseops.linop.spmv_csr, linop.py:102-121).  Every entry
+ * point replaces the reference function cited beside it; INTEGRATION.md shows the
+ * ctypes binding a maintainer adds on the reference side.
+ *
+ * Conventions
+ *   - Memory: every pointer in a struct below is DEVICE memory owned by the caller
+ *     (the Python frontend allocates it with torch); the library never allocates
+ *     device memory.  Host-side structs are passed by pointer and only read during the
+ *     call.  Workspace sizes are queried with sb_*_workspace_bytes.
+ *   - Streams: all work is enqueued on the caller's `stream` (a cudaStream_t; 0 = the
+ *     legacy default stream).  SpMV / BLAS-1 updates return without synchronising;
+ *     calls that must return a host value (dot, norm2, solvers, row stats) synchronise
+ *     the stream before returning.
+ *   - Errors: every call returns an sb_status whose codes map 1:1 onto the reference's
+ *     exception kinds (sparseops/errors.py:8-131); `err` (nullable) receives the code,
+ *     the failing row / iteration and a message.
+ *   - Numerics: fp64 accumulation, fp32 products rounded before the add, no FMA,
+ *     deterministic reductions (see paper_2510_08230_b200/csrc/common.cuh).
+ */
+#ifndef SPARSEB200_H
+#define SPARSEB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* exported even when the library is compiled with -fvisibility=hidden */
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+typedef void *sb_stream_t; /* cudaStream_t */
+
+/* status codes <-> reference exception kinds (sparseops/errors.py) */
+typedef enum {
+    SB_OK = 0,
+    SB_ERR_INVALID_ARGUMENT = 1,   /* InvalidArgumentError      "invalid-argument"   errors.py:14 */
+    SB_ERR_DIMENSION_MISMATCH = 2, /* DimensionMismatchError    "dimension-mismatch" errors.py:31 */
+    SB_ERR_PRECISION_MISMATCH = 3, /* PrecisionMismatchError    "precision-mismatch" errors.py:35 */
+    SB_ERR_UNSUPPORTED = 4,        /* UnsupportedFeatureError   "unsupported-feature" errors.py:27 */
+    SB_ERR_INDEX_BOUNDS = 5,       /* IndexBoundsError (row = offending triplet)     errors.py:39 */
+    SB_ERR_BREAKDOWN = 6,          /* BreakdownError (iteration)                     errors.py:85-93 */
+    SB_ERR_NUMERIC_FAILURE = 7,    /* NumericFailureError                            errors.py:96 */
+    SB_ERR_SINGULAR_DIAGONAL = 8,  /* SingularDiagonalError (row)                    errors.py:115-121 */
+    SB_ERR_CUDA = 9,               /* CUDA runtime failure (no reference analogue) */
+    SB_ERR_NCCL = 10               /* NCCL failure (multi-GPU only) */
+} sb_status;
+
+typedef struct {
+    int32_t code;
+    int32_t pad;
+    int64_t row;       /* SingularDiagonalError.row / IndexBoundsError triplet */
+    int64_t iteration; /* BreakdownError.iteration */
+    char msg[256];
+} sb_error;
+
+/* core.DenseMatrix (core.py:226-301): row-major, element (i, j) at data[i*stride + j]. */
+typedef struct {
+    void *data;
+    int64_t rows, cols, stride;
+} sb_dense;
+
+/* ------------------------------------------------------------------ sparse formats */
+/* CSR SpMV kernel selection (filled by sb_csr_plan_select from row statistics). */
+enum {
+    SB_CSR_AUTO = 0,
+    SB_CSR_STRICT = 1, /* thread per row, global loads: the reference loop on the device */
+    SB_CSR_STREAM = 2, /* TMA-staged row blocks, thread per row (regular rows; bit-exact) */
+    SB_CSR_VECTOR = 3, /* sub-warp per row (long regular rows) */
+    SB_CSR_MERGE = 4   /* load-balanced merge-path (irregular rows) */
+};
+
+typedef struct {
+    int64_t rows, nnz, min_len, max_len, empty_rows;
+    double mean_len, std_len;
+    int64_t max_block_nnz[4]; /* max nnz over aligned blocks of 32, 64, 128, 256 rows */
+} sb_row_stats;
+
+typedef struct {
+    int32_t kernel;         /* SB_CSR_* */
+    int32_t block_rows;     /* stream: rows per block R; vector: lanes per row */
+    int32_t nnz_cap;        /* stream: max nnz of one R-row block */
+    int32_t pad;
+    int64_t num_tiles;      /* merge: tiles of items_per_tile merge items */
+    int64_t items_per_tile;
+    void *tile_rows;        /* merge: int64[num_tiles + 1] */
+    void *tile_nnz;         /* merge: int64[num_tiles + 1] */
+    void *carry_rows;       /* merge: int64[num_tiles] */
+    void *carry_vals;       /* merge: double[num_tiles] */
+} sb_csr_plan;
+
+/* formats.CsrMatrix (formats.py:84-128) */
+typedef struct {
+    int64_t rows, cols, nnz;
+    const void *row_ptrs, *col_idxs, *values;
+    const sb_csr_plan *plan;
+} sb_csr;
+
+typedef struct {
+    int64_t num_tiles; /* ceil(nnz / sb_coo_tile_entries()) */
+    void *carry_rows;  /* int64[num_tiles] */
+    void *carry_vals;  /* double[num_tiles] */
+} sb_coo_plan;
+
+/* formats.CooMatrix (formats.py:57-81): canonical (sorted, unique) entries */
+typedef struct {
+    int64_t rows, cols, nnz;
+    const void *row_idxs, *col_idxs, *values;
+    const sb_coo_plan *plan;
+} sb_coo;
+
+/* ELL(width, stride): entry k of row i at k*stride + i; padding col = -1, val = 0.
+ * (absent from the reference; layout pinned in SURVEY.md §8) */
+typedef struct {
+    int64_t rows, cols, width, stride;
+    const void *col_idxs, *values;
+} sb_ell;
+
+/* SELL-P(slice_size): entry k of row i (slice s = i / S) at (slice_sets[s] + k)*S + i%S */
+typedef struct {
+    int64_t rows, cols, slice_size, num_slices;
+    const void *slice_lengths, *slice_sets, *col_idxs, *values;
+} sb_sellp;
+
+/* Hybrid(w): the first min(len_i, w) entries of each row in ELL(w), the rest in COO */
+typedef struct {
+    sb_ell ell;
+    sb_coo coo;
+} sb_hybrid;
+
+enum { SB_FMT_CSR = 0, SB_FMT_COO = 1, SB_FMT_ELL = 2, SB_FMT_SELLP = 3, SB_FMT_HYBRID = 4 };
+
+/* a LinOp (linop.py:44-73) of any storage format */
+typedef struct {
+    int32_t format; /* SB_FMT_* */
+    int32_t pad;
+    const void *mat; /* sb_csr* / sb_coo* / sb_ell* / sb_sellp* / sb_hybrid* */
+} sb_matrix;
+
+/* ------------------------------------------------------------------ solvers */
+/* solvers.Iteration / ResidualNorm (solvers.py:52-76) reduced to OR semantics:
+ * stop when it >= max_iters (min over Iteration entries) or, if has_residual,
+ * when ||r|| <= reduction_factor * ||b|| (max over ResidualNorm entries; absolute if
+ * ||b|| == 0).  check_criteria, solvers.py:121-135. */
+typedef struct {
+    int64_t max_iters;
+    int32_t has_residual;
+    int32_t pad;
+    double reduction_factor;
+} sb_criteria;
+
+/* solvers.ConvergenceLog (solvers.py:79-87); history is a HOST buffer of history_cap
+ * doubles filled with one residual per criteria check. */
+typedef struct {
+    int64_t iterations;
+    int32_t converged;
+    int32_t stop_reason; /* 0 "residual", 1 "max_iters" */
+    int64_t history_len;
+    double *history;
+    int64_t history_cap;
+} sb_log;
+
+/* library / device */
+int sb_version(void);
+const char *sb_status_string(int code);
+/* CUDA graph + conditional-node solver loop (1, default) or host-polled launches (0) */
+void sb_set_graph_mode(int enabled);
+
+#define SB_VALUE_DECLS(VN)                                                                       \
+    /* core.dot / norm2 / axpy / scal / copy_into (core.py:358-401); jacobi apply (precond.py:57-63) */ \
+    sb_status sb_dot_##VN(const sb_dense *x, const sb_dense *y, double *out, void *workspace,     \
+                          sb_stream_t stream, sb_error *err);                                     \
+    sb_status sb_norm2_##VN(const sb_dense *x, double *out, void *workspace, sb_stream_t stream,  \
+                            sb_error *err);                                                       \
+    sb_status sb_axpy_##VN(double alpha, const sb_dense *x, sb_dense *y, sb_stream_t stream,      \
+                           sb_error *err);                                                        \
+    sb_status sb_scal_##VN(double alpha, sb_dense *x, sb_stream_t stream, sb_error *err);         \
+    sb_status sb_copy_##VN(const sb_dense *src, sb_dense *dst, sb_stream_t stream, sb_error *err); \
+    sb_status sb_fill_##VN(sb_dense *x, double value, sb_stream_t stream, sb_error *err);         \
+    sb_status sb_jacobi_apply_##VN(const void *inv_diag, const sb_dense *b, sb_dense *x,          \
+                                   sb_stream_t stream, sb_error *err);
+
+#define SB_INDEX_DECLS(VN, IN)                                                                    \
+    /* SpMV x = A b: linop.spmv_csr / spmv_coo (linop.py:102-159) and the formats the            \
+       reference lacks (ELL / SELL-P / Hybrid) */                                    \
+    sb_status sb_csr_spmv_##VN##_##IN(const sb_csr *a, const sb_dense *b, sb_dense *x,            \
+                                      sb_stream_t stream, sb_error *err);                         \
+    sb_status sb_coo_spmv_##VN##_##IN(const sb_coo *a, const sb_dense *b, sb_dense *x,            \
+                                      sb_stream_t stream, sb_error *err);                         \
+    sb_status sb_ell_spmv_##VN##_##IN(const sb_ell *a, const sb_dense *b, sb_dense *x,            \
+                                      sb_stream_t stream, sb_error *err);                         \
+    sb_status sb_sellp_spmv_##VN##_##IN(const sb_sellp *a, const sb_dense *b, sb_dense *x,        \
+                                        sb_stream_t stream, sb_error *err);                       \
+    sb_status sb_hybrid_spmv_##VN##_##IN(const sb_hybrid *a, const sb_dense *b, sb_dense *x,      \
+                                         sb_stream_t stream, sb_error *err);                      \
+    /* LinOp.apply_advanced x = alpha A b + beta x (linop.py:81-99); tmp: rows x cols workspace */ \
+    sb_status sb_apply_advanced_##VN##_##IN(const sb_matrix *a, double alpha, const sb_dense *b,  \
+                                            double beta, sb_dense *x, void *tmp,                  \
+                                            sb_stream_t stream, sb_error *err);                   \
+    /* jacobi_create (precond.py:66-84) incl. CsrMatrix.diagonal (formats.py:113-122) */          \
+    sb_status sb_jacobi_create_##VN##_##IN(const sb_csr *a, void *inv_diag, void *workspace,     \
+                                           sb_stream_t stream, sb_error *err);                    \
+    /* format conversions (formats.py:184-199 + canonical layouts of SURVEY.md §8) */             \
+    sb_status sb_ell_from_csr_##VN##_##IN(const sb_csr *a, sb_ell *out, sb_stream_t stream,       \
+                                          sb_error *err);                                         \
+    sb_status sb_sellp_from_csr_##VN##_##IN(const sb_csr *a, sb_sellp *out, sb_stream_t stream,   \
+                                            sb_error *err);                                       \
+    sb_status sb_hybrid_from_csr_##VN##_##IN(const sb_csr *a, const void *coo_row_ptrs,           \
+                                             sb_hybrid *out, sb_stream_t stream, sb_error *err);  \
+    /* coo_from_arrays (formats.py:131-166): canonicalise raw int64 triplets on the device.       \
+       Returns the canonical nnz in *nnz_out; out arrays sized for the raw count. */              \
+    sb_status sb_coo_from_arrays_##VN##_##IN(int64_t rows, int64_t cols, int64_t count,           \
+                                             const int64_t *row_idxs, const int64_t *col_idxs,    \
+                                             const void *values, void *out_rows, void *out_cols,  \
+                                             void *out_vals, void *workspace,                     \
+                                             size_t workspace_bytes, int64_t *nnz_out,            \
+                                             sb_stream_t stream, sb_error *err);                  \
+    /* solvers: Cg (solvers.py:188-224), Cgs (:231-284), Gmres (:322-399), BiCGSTAB (new) */      \
+    sb_status sb_cg_solve_##VN##_##IN(const sb_matrix *a, const void *inv_diag,                   \
+                                      const sb_dense *b, sb_dense *x, const sb_criteria *crit,    \
+                                      void *workspace, sb_log *log, sb_stream_t stream,           \
+                                      sb_error *err);                                             \
+    sb_status sb_cgs_solve_##VN##_##IN(const sb_matrix *a, const void *inv_diag,                  \
+                                       const sb_dense *b, sb_dense *x, const sb_criteria *crit,   \
+                                       void *workspace, sb_log *log, sb_stream_t stream,          \
+                                       sb_error *err);                                            \
+    sb_status sb_bicgstab_solve_##VN##_##IN(const sb_matrix *a, const void *inv_diag,             \
+                                            const sb_dense *b, sb_dense *x,                       \
+                                            const sb_criteria *crit, void *workspace,             \
+                                            sb_log *log, sb_stream_t stream, sb_error *err);      \
+    sb_status sb_gmres_solve_##VN##_##IN(const sb_matrix *a, const void *inv_diag,                \
+                                         const sb_dense *b, sb_dense *x, const sb_criteria *crit, \
+                                         int64_t krylov_dim, void *workspace, sb_log *log,        \
+                                         sb_stream_t stream, sb_error *err);
+
+SB_VALUE_DECLS(float)
+SB_VALUE_DECLS(double)
+SB_INDEX_DECLS(float, i32)
+SB_INDEX_DECLS(float, i64)
+SB_INDEX_DECLS(double, i32)
+SB_INDEX_DECLS(double, i64)
+
+/* index-only operations */
+#define SB_IDX_DECLS(IN)                                                                          \
+    /* row-length statistics (drive the CSR kernel choice); workspace: 256 bytes */              \
+    sb_status sb_csr_row_stats_##IN(int64_t rows, const void *row_ptrs, void *workspace,          \
+                                    sb_row_stats *out, sb_stream_t stream, sb_error *err);        \
+    /* fill plan->tile_* for the merge-path kernel (plan from sb_csr_plan_select) */              \
+    sb_status sb_csr_plan_build_##IN(int64_t rows, int64_t nnz, const void *row_ptrs,            \
+                                     sb_csr_plan *plan, sb_stream_t stream, sb_error *err);       \
+    /* csr_from_coo (formats.py:184-191): row_ptrs from sorted row indices */                     \
+    sb_status sb_csr_row_ptrs_from_coo_##IN(int64_t rows, int64_t nnz, const void *row_idxs,      \
+                                            void *row_ptrs, sb_stream_t stream, sb_error *err);   \
+    /* coo_from_csr (formats.py:194-199): expand row_ptrs into row indices */                     \
+    sb_status sb_coo_row_idxs_from_csr_##IN(int64_t rows, int64_t nnz, const void *row_ptrs,      \
+                                            void *row_idxs, sb_stream_t stream, sb_error *err);   \
+    /* SELL-P slice metadata (slice_lengths, slice_sets) and ELL / Hybrid widths */               \
+    sb_status sb_sellp_slices_##IN(int64_t rows, const void *row_ptrs, int64_t slice_size,        \
+                                   void *slice_lengths, void *slice_sets, int64_t *total,         \
+                                   sb_stream_t stream, sb_error *err);                            \
+    /* Hybrid: per-row COO-tail counts as row_ptrs of the tail (length rows+1), total returned */ \
+    sb_status sb_hybrid_tail_ptrs_##IN(int64_t rows, const void *row_ptrs, int64_t width,         \
+                                       void *tail_ptrs, int64_t *tail_nnz, sb_stream_t stream,    \
+                                       sb_error *err);                                            \
+    /* synthetic stencil generators straight into canonical CSR:                 \
+       dim 2 -> 5-point Poisson, dim 3 -> 7-point with convection c (0 = Poisson) */              \
+    sb_status sb_stencil_csr_double_##IN(int64_t p, int32_t dim, double c, void *row_ptrs,       \
+                                         void *col_idxs, void *values, sb_stream_t stream,        \
+                                         sb_error *err);                                          \
+    sb_status sb_stencil_csr_float_##IN(int64_t p, int32_t dim, double c, void *row_ptrs,        \
+                                        void *col_idxs, void *values, sb_stream_t stream,         \
+                                        sb_error *err);
+
+SB_IDX_DECLS(i32)
+SB_IDX_DECLS(i64)
+
+/* host-side CSR kernel choice from row statistics (force = SB_CSR_* or SB_CSR_AUTO);
+ * fills plan->kernel/block_rows/nnz_cap/num_tiles/items_per_tile.  The caller then
+ * allocates the tile/carry buffers (when num_tiles > 0) and calls sb_csr_plan_build. */
+sb_status sb_csr_plan_select(const sb_row_stats *stats, int32_t value_bytes, int32_t index_bytes,
+                             int32_t force, sb_csr_plan *plan, sb_error *err);
+/* COO tile size (entries per carry slot) */
+int64_t sb_coo_tile_entries(void);
+/* workspace sizes (bytes) */
+size_t sb_reduce_workspace_bytes(void);
+size_t sb_coo_from_arrays_workspace_bytes(int64_t count);
+size_t sb_solver_workspace_bytes(int32_t solver, int32_t value_bytes, int64_t n, int64_t krylov_dim,
+                                 int64_t history_cap);
+
+/* solver ids for sb_solver_workspace_bytes */
+enum { SB_SOLVER_CG = 0, SB_SOLVER_CGS = 1, SB_SOLVER_GMRES = 2, SB_SOLVER_BICGSTAB = 3 };
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPARSEB200_H */

@@ -1,0 +1,197 @@
+// bicgstab.cu -- right-preconditioned BiCGSTAB on the device (recurrence in oracle/sbref.cpp).
+#include <cmath>
+
+#include "solver_common.cuh"
+
+namespace sb {
+
+// ================================================================ BiCGSTAB
+struct SkipEarly {
+    __device__ __forceinline__ bool skip(const Ctl *c) const { return c->early != 0; }
+    __device__ __forceinline__ void prepare(const Ctl *) {}
+};
+
+// p = r (first) or p = r + beta (p - omega v) as axpy(-omega,v,p); scal(beta,p); axpy(1,r,p);
+// phat = M p
+template <class V>
+struct BiDirection : SkipNone {
+    const V *r, *v, *inv;
+    V *p, *ph;
+    double beta, omega;
+    bool first;
+    __device__ __forceinline__ void prepare(const Ctl *c) {
+        beta = c->beta;
+        omega = c->omega;
+        first = c->iter == 0;
+    }
+    __device__ __forceinline__ void elem(int64_t i, double (&)[1]) const {
+        V pi;
+        if (first) pi = r[i];
+        else pi = axpy_e(1.0, r[i], scal_e(beta, axpy_e(-omega, v[i], p[i])));
+        p[i] = pi;
+        ph[i] = precond_e(inv, i, pi);
+    }
+};
+
+// s = r - alpha v; shat = M s; ||s|| may stop early (x += alpha phat follows)
+template <class V>
+struct BiS : SkipNone {
+    const V *r, *v, *inv;
+    V *s, *sh;
+    double alpha;
+    __device__ __forceinline__ void prepare(const Ctl *c) { alpha = c->alpha; }
+    __device__ __forceinline__ void elem(int64_t i, double (&part)[1]) const {
+        const V si = axpy_e(-alpha, v[i], r[i]);
+        s[i] = si;
+        sh[i] = precond_e(inv, i, si);
+        part[0] = addd(part[0], mulp(si, si));
+    }
+    __device__ __forceinline__ void last(Ctl *c, const double (&tot)[1]) const {
+        const double snorm = sqrt(tot[0]);
+        c->snorm = snorm;
+        if (c->has_rf && check_criteria(c, c->iter, snorm, c->bnorm) == STOP_RESIDUAL) {
+            record(c, c->iter, snorm);
+            c->early = 1;
+        }
+    }
+};
+
+// early stop: x += alpha phat, then finish
+template <class V>
+struct BiEarlyX {
+    const V *ph;
+    V *x;
+    double alpha;
+    __device__ __forceinline__ bool skip(const Ctl *c) const { return c->early == 0; }
+    __device__ __forceinline__ void prepare(const Ctl *c) { alpha = c->alpha; }
+    __device__ __forceinline__ void elem(int64_t i, double (&part)[1]) const {
+        x[i] = axpy_e(alpha, ph[i], x[i]);
+        (void)part;
+    }
+    __device__ __forceinline__ void last(Ctl *c, const double (&)[1]) const {
+        finish_with(c, c->iter, STOP_RESIDUAL);
+    }
+};
+
+// t = A shat with t.t and s.t -> omega
+struct BiOmegaFin {
+    __device__ __forceinline__ bool skip(const Ctl *c) const { return c->early != 0; }
+    __device__ __forceinline__ void last(Ctl *c, const double (&tot)[2]) const {
+        const double tt = tot[0], ts = tot[1];
+        if (!isfinite(tt) || !isfinite(ts) || tt == 0.0) {
+            breakdown(c, c->iter);
+            return;
+        }
+        c->omega = ts / tt;
+    }
+};
+
+// x += alpha phat + omega shat; r = s - omega t; dots r.r, rhat.r (next rho)
+template <class V>
+struct BiUpdate : SkipEarly {
+    const V *ph, *sh, *s, *t, *rh;
+    V *x, *r;
+    double alpha, omega;
+    __device__ __forceinline__ void prepare(const Ctl *c) {
+        alpha = c->alpha;
+        omega = c->omega;
+    }
+    __device__ __forceinline__ void elem(int64_t i, double (&part)[2]) const {
+        x[i] = axpy_e(omega, sh[i], axpy_e(alpha, ph[i], x[i]));
+        const V ri = axpy_e(-omega, t[i], s[i]);
+        r[i] = ri;
+        part[0] = addd(part[0], mulp(ri, ri));
+        part[1] = addd(part[1], mulp(rh[i], ri));
+    }
+    __device__ __forceinline__ void last(Ctl *c, const double (&tot)[2]) const {
+        const int64_t it = c->iter;
+        const double rnorm = sqrt(tot[0]);
+        c->rnorm = rnorm;
+        record(c, it, rnorm);
+        int reason = check_criteria(c, it, rnorm, c->bnorm);
+        if (reason == STOP_NONE && rnorm == 0.0) reason = STOP_RESIDUAL;
+        if (reason != STOP_NONE) {
+            finish_with(c, it, reason);
+            return;
+        }
+        if (c->omega == 0.0) {
+            breakdown(c, it);
+            return;
+        }
+        const double rho = tot[1];
+        if (!isfinite(rho) || fabs(rho) <= kBreakdownRtol * c->shadow_norm * rnorm) {
+            breakdown(c, it + 1);
+            return;
+        }
+        c->rho_prev = c->rho;
+        c->rho = rho;
+        c->beta = (rho / c->rho_prev) * (c->alpha / c->omega);
+    }
+};
+
+template <class V, class I>
+sb_status bicgstab_solve(const SolveArgs &a) {
+    sb_error *err = a.err;
+    int64_t n = 0;
+    sb_status s = check_solve_args<V>(a, n);
+    if (s != SB_OK) return s;
+    const int64_t cap = a.log->history_cap;
+    SolverWs w = carve_ws(a.ws, SB_SOLVER_BICGSTAB, sizeof(V), n, 0, cap);
+    V *r = ws_vec<V>(w, 0), *rh = ws_vec<V>(w, 1), *p = ws_vec<V>(w, 2), *v = ws_vec<V>(w, 3),
+      *sv = ws_vec<V>(w, 4), *ph = ws_vec<V>(w, 5), *sh = ws_vec<V>(w, 6), *t = ws_vec<V>(w, 7);
+    const V *b = (const V *)a.b->data, *inv = (const V *)a.inv;
+    V *x = (V *)a.x->data;
+    Ctl *ctl = w.ctl;
+    double *part = w.partials;
+    const sb_matrix M = *a.A;
+    Ctl h = initial_ctl(*a.crit, w, cap);
+    LoopSpec spec;
+    spec.key = "bicgstab" + std::to_string(sizeof(V)) + std::to_string(sizeof(I)) + "|" +
+               matrix_key(M) + ptr_key({a.inv, b, x, a.ws});
+    spec.poll_chunk = 8;
+    spec.setup = [=](cudaStream_t st) -> cudaError_t {
+        cudaError_t e = matrix_apply<V, I>(M, x, 1, t, 1, EpiStore<V>{t, 1}, st);
+        if (e != cudaSuccess) return e;
+        return launch_ew<2>(n, ctl, part, ShadowInit<V>{{}, b, t, r, rh}, st);
+    };
+    spec.body = [=](cudaStream_t st) -> cudaError_t {
+        cudaError_t e = launch_ew<0>(n, ctl, part, BiDirection<V>{{}, r, v, inv, p, ph, 0, 0, false}, st);
+        if (e != cudaSuccess) return e;
+        e = matrix_apply<V, I>(M, ph, 1, v, 1, EpiSolver<V, 1, BiSigmaFin>{v, rh, nullptr, ctl, part, {}}, st);
+        if (e != cudaSuccess) return e;
+        e = launch_ew<1>(n, ctl, part, BiS<V>{{}, r, v, inv, sv, sh, 0}, st);
+        if (e != cudaSuccess) return e;
+        e = launch_ew<1>(n, ctl, part, BiEarlyX<V>{ph, x, 0}, st);
+        if (e != cudaSuccess) return e;
+        e = matrix_apply<V, I>(M, sh, 1, t, 1, EpiSolver<V, 2, BiOmegaFin>{t, nullptr, sv, ctl, part, {}}, st);
+        if (e != cudaSuccess) return e;
+        return launch_ew<2>(n, ctl, part, BiUpdate<V>{{}, ph, sh, sv, t, rh, x, r, 0, 0}, st);
+    };
+    s = run_loop(spec, ctl, h, a.st, err);
+    if (s != SB_OK) return s;
+    return finish_log(h, a, w);
+}
+
+}  // namespace sb
+
+using namespace sb;
+
+extern "C" {
+
+#define SB_DEFS(V, VN, I, IN) \
+    sb_status sb_bicgstab_solve_##VN##_##IN(const sb_matrix *a, const void *inv_diag,              \
+                                            const sb_dense *b, sb_dense *x,                        \
+                                            const sb_criteria *crit, void *workspace, sb_log *log, \
+                                            sb_stream_t stream, sb_error *err) {                   \
+        SB_GUARD_BEGIN                                                                             \
+        return bicgstab_solve<V, I>(SolveArgs{a, inv_diag, b, x, crit, 0, workspace, log,          \
+                                              as_stream(stream), err});                            \
+        SB_GUARD_END                                                                               \
+    }
+
+SB_DEFS(float, float, int32_t, i32)
+SB_DEFS(float, float, int64_t, i64)
+SB_DEFS(double, double, int32_t, i32)
+SB_DEFS(double, double, int64_t, i64)
+
+}  // extern "C"

@@ -1,0 +1,167 @@
+// cg.cu -- preconditioned CG on the device (solvers.py:188-224): 3 fused kernels per iteration.
+#include <cmath>
+
+#include "solver_common.cuh"
+
+namespace sb {
+
+// ================================================================ CG
+// setup: r = b - A x (t = A x first), z = M r, p = z; dots b.b, r.r, r.z
+template <class V>
+struct CgInit : SkipNone {
+    const V *b, *t, *inv;
+    V *r, *z, *p;
+    __device__ __forceinline__ void elem(int64_t i, double (&part)[3]) const {
+        const V bi = b[i];
+        const V ri = axpy_e(-1.0, t[i], bi);
+        const V zi = precond_e(inv, i, ri);
+        r[i] = ri;
+        z[i] = zi;
+        p[i] = zi;
+        part[0] = addd(part[0], mulp(bi, bi));
+        part[1] = addd(part[1], mulp(ri, ri));
+        part[2] = addd(part[2], mulp(ri, zi));
+    }
+    __device__ __forceinline__ void last(Ctl *c, const double (&tot)[3]) const {
+        c->bnorm = sqrt(tot[0]);
+        c->rnorm = sqrt(tot[1]);
+        c->iter = 0;
+        if (c->rnorm == 0.0) {  // _exact_log (solvers.py:179-181)
+            c->exact = 1;
+            c->converged = 1;
+            c->stop_reason = STOP_RESIDUAL;
+            if (c->hist_cap > 0) c->hist[0] = 0.0;
+            c->hist_len = 1;
+            stop_loop(c);
+            return;
+        }
+        c->rz = tot[2];
+    }
+};
+
+// q = A p, fused p.q -> alpha (solvers.py:202-206)
+struct CgPqFin {
+    __device__ __forceinline__ bool skip(const Ctl *) const { return false; }
+    __device__ __forceinline__ void last(Ctl *c, const double (&tot)[1]) const {
+        const int64_t it = c->iter + 1;
+        c->iter = it;
+        const double pq = tot[0];
+        if (!isfinite(pq) || pq <= kBreakdownRtol * fabs(c->rz)) {
+            breakdown(c, it);
+            return;
+        }
+        c->alpha = c->rz / pq;
+    }
+};
+
+// x += alpha p; r -= alpha q; z = M r; dots r.r, r.z -> criteria, beta (solvers.py:207-222)
+template <class V>
+struct CgUpdate : SkipNone {
+    const V *p, *q, *inv;
+    V *x, *r, *z;
+    double alpha;
+    __device__ __forceinline__ void prepare(const Ctl *c) { alpha = c->alpha; }
+    __device__ __forceinline__ void elem(int64_t i, double (&part)[2]) const {
+        x[i] = axpy_e(alpha, p[i], x[i]);
+        const V ri = axpy_e(-alpha, q[i], r[i]);
+        const V zi = precond_e(inv, i, ri);
+        r[i] = ri;
+        z[i] = zi;
+        part[0] = addd(part[0], mulp(ri, ri));
+        part[1] = addd(part[1], mulp(ri, zi));
+    }
+    __device__ __forceinline__ void last(Ctl *c, const double (&tot)[2]) const {
+        const int64_t it = c->iter;
+        const double rnorm = sqrt(tot[0]);
+        c->rnorm = rnorm;
+        record(c, it, rnorm);
+        int reason = check_criteria(c, it, rnorm, c->bnorm);
+        if (reason == STOP_NONE && rnorm == 0.0) reason = STOP_RESIDUAL;
+        if (reason != STOP_NONE) {
+            finish_with(c, it, reason);
+            return;
+        }
+        const double rz_new = tot[1];
+        if (!isfinite(rz_new) || c->rz == 0.0) {
+            breakdown(c, it);
+            return;
+        }
+        c->beta = rz_new / c->rz;
+        c->rz = rz_new;
+    }
+};
+
+// p = z + beta p  (scal(beta, p); axpy(1, z, p))
+template <class V>
+struct CgDirection : SkipNone {
+    const V *z;
+    V *p;
+    double beta;
+    __device__ __forceinline__ void prepare(const Ctl *c) { beta = c->beta; }
+    __device__ __forceinline__ void elem(int64_t i, double (&)[1]) const {
+        p[i] = axpy_e(1.0, z[i], scal_e(beta, p[i]));
+    }
+};
+
+template <class V, class I>
+sb_status cg_solve(const SolveArgs &a) {
+    sb_error *err = a.err;
+    int64_t n = 0;
+    sb_status s = check_solve_args<V>(a, n);
+    if (s != SB_OK) return s;
+    const int64_t cap = a.log->history_cap;
+    SolverWs w = carve_ws(a.ws, SB_SOLVER_CG, sizeof(V), n, 0, cap);
+    V *r = ws_vec<V>(w, 0), *z = ws_vec<V>(w, 1), *p = ws_vec<V>(w, 2), *q = ws_vec<V>(w, 3),
+      *t = ws_vec<V>(w, 4);
+    const V *b = (const V *)a.b->data, *inv = (const V *)a.inv;
+    V *x = (V *)a.x->data;
+    Ctl *ctl = w.ctl;
+    double *part = w.partials;
+    const sb_matrix M = *a.A;
+    Ctl h = initial_ctl(*a.crit, w, cap);
+    LoopSpec spec;
+    spec.key = "cg" + std::to_string(sizeof(V)) + std::to_string(sizeof(I)) + "|" + matrix_key(M) +
+               ptr_key({a.inv, b, x, a.ws});
+    spec.poll_chunk = 8;
+    spec.setup = [=](cudaStream_t st) -> cudaError_t {
+        cudaError_t e = matrix_apply<V, I>(M, x, 1, t, 1, EpiStore<V>{t, 1}, st);
+        if (e != cudaSuccess) return e;
+        return launch_ew<3>(n, ctl, part, CgInit<V>{{}, b, t, inv, r, z, p}, st);
+    };
+    spec.body = [=](cudaStream_t st) -> cudaError_t {
+        cudaError_t e = matrix_apply<V, I>(
+            M, p, 1, q, 1, EpiSolver<V, 1, CgPqFin>{q, p, nullptr, ctl, part, CgPqFin{}}, st);
+        if (e != cudaSuccess) return e;
+        e = launch_ew<2>(n, ctl, part, CgUpdate<V>{{}, p, q, inv, x, r, z, 0.0}, st);
+        if (e != cudaSuccess) return e;
+        return launch_ew<0>(n, ctl, part, CgDirection<V>{{}, z, p, 0.0}, st);
+    };
+    s = run_loop(spec, ctl, h, a.st, err);
+    if (s != SB_OK) return s;
+    return finish_log(h, a, w);
+}
+
+
+}  // namespace sb
+
+using namespace sb;
+
+extern "C" {
+
+#define SB_DEFS(V, VN, I, IN) \
+    sb_status sb_cg_solve_##VN##_##IN(const sb_matrix *a, const void *inv_diag,                    \
+                                      const sb_dense *b, sb_dense *x, const sb_criteria *crit,     \
+                                      void *workspace, sb_log *log, sb_stream_t stream,            \
+                                      sb_error *err) {                                             \
+        SB_GUARD_BEGIN                                                                             \
+        return cg_solve<V, I>(SolveArgs{a, inv_diag, b, x, crit, 0, workspace, log,                \
+                                        as_stream(stream), err});                                  \
+        SB_GUARD_END                                                                               \
+    }
+
+SB_DEFS(float, float, int32_t, i32)
+SB_DEFS(float, float, int64_t, i64)
+SB_DEFS(double, double, int32_t, i32)
+SB_DEFS(double, double, int64_t, i64)
+
+}  // extern "C"

@@ -1,0 +1,194 @@
+// cgs.cu -- CGS on the device (solvers.py:231-284) with the residual update fused into the SpMV.
+#include <cmath>
+
+#include "solver_common.cuh"
+
+namespace sb {
+
+// ================================================================ CGS (solvers.py:231-284)
+// u = r, p = u (first) | u = r + beta q; p = u + beta (q + beta p) with the reference's
+// copy/scal/axpy rounding; phat = M p
+template <class V>
+struct CgsDirection : SkipNone {
+    const V *r, *q, *inv;
+    V *u, *p, *ph;
+    double beta;
+    bool first;
+    __device__ __forceinline__ void prepare(const Ctl *c) {
+        beta = c->beta;
+        first = c->iter == 0;
+    }
+    __device__ __forceinline__ void elem(int64_t i, double (&)[1]) const {
+        V ui, pi;
+        if (first) {
+            ui = r[i];
+            pi = ui;
+        } else {
+            const V qi = q[i];
+            ui = axpy_e(1.0, r[i], scal_e(beta, qi));
+            pi = axpy_e(1.0, ui, axpy_e(beta, qi, scal_e(__dmul_rn(beta, beta), p[i])));
+        }
+        u[i] = ui;
+        p[i] = pi;
+        ph[i] = precond_e(inv, i, pi);
+    }
+};
+
+// q = u - alpha v; uhat = M (u + q); x += alpha uhat
+template <class V>
+struct CgsQ : SkipNone {
+    const V *u, *v, *inv;
+    V *q, *uh, *x;
+    double alpha;
+    __device__ __forceinline__ void prepare(const Ctl *c) { alpha = c->alpha; }
+    __device__ __forceinline__ void elem(int64_t i, double (&)[1]) const {
+        const V ui = u[i];
+        const V qi = axpy_e(-alpha, v[i], ui);
+        const V uq = axpy_e(1.0, qi, ui);
+        const V uhi = precond_e(inv, i, uq);
+        q[i] = qi;
+        uh[i] = uhi;
+        x[i] = axpy_e(alpha, uhi, x[i]);
+    }
+};
+
+// SpMV epilogue: t = A uhat row by row, immediately r -= alpha t with dots r.r and rs.r
+template <class V>
+struct EpiCgsResidual {
+    static constexpr int N = 2;
+    V *t, *r;
+    const V *rs;
+    Ctl *ctl;
+    double *partials;
+    __device__ __forceinline__ bool skip() const { return ctl->done != 0; }
+    __device__ __forceinline__ void row(int64_t i, double acc, double (&part)[N]) const {
+        const V ti = (V)acc;
+        t[i] = ti;
+        const V ri = axpy_e(-ctl->alpha, ti, r[i]);
+        r[i] = ri;
+        part[0] = addd(part[0], mulp(ri, ri));
+        part[1] = addd(part[1], mulp(rs[i], ri));
+    }
+    __device__ __forceinline__ void finish(double (&part)[N]) const {
+        double tot[N];
+        if (grid_reduce<N>(part, partials, &ctl->ticket[0], tot) && threadIdx.x == 0) last(ctl, tot);
+    }
+    __device__ __forceinline__ static void last(Ctl *c, const double (&tot)[2]) {
+        const int64_t it = c->iter;
+        const double rnorm = sqrt(tot[0]);
+        c->rnorm = rnorm;
+        record(c, it, rnorm);
+        int reason = check_criteria(c, it, rnorm, c->bnorm);
+        if (reason == STOP_NONE && rnorm == 0.0) reason = STOP_RESIDUAL;
+        if (reason != STOP_NONE) {
+            finish_with(c, it, reason);
+            return;
+        }
+        const double rho = tot[1];
+        if (!isfinite(rho) || fabs(rho) <= kBreakdownRtol * c->shadow_norm * rnorm) {
+            breakdown(c, it + 1);
+            return;
+        }
+        c->rho_prev = c->rho;
+        c->rho = rho;
+        c->beta = rho / c->rho_prev;
+    }
+};
+
+// the same update as a separate pass for row-splitting formats (t already written)
+template <class V>
+struct CgsResidualPass : SkipNone {
+    const V *t, *rs;
+    V *r;
+    double alpha;
+    __device__ __forceinline__ void prepare(const Ctl *c) { alpha = c->alpha; }
+    __device__ __forceinline__ void elem(int64_t i, double (&part)[2]) const {
+        const V ri = axpy_e(-alpha, t[i], r[i]);
+        r[i] = ri;
+        part[0] = addd(part[0], mulp(ri, ri));
+        part[1] = addd(part[1], mulp(rs[i], ri));
+    }
+    __device__ __forceinline__ void last(Ctl *c, const double (&tot)[2]) const {
+        EpiCgsResidual<V>::last(c, tot);
+    }
+};
+
+inline bool row_owned_format(const sb_matrix &M) {
+    if (M.format == SB_FMT_ELL || M.format == SB_FMT_SELLP) return true;
+    if (M.format == SB_FMT_CSR) {
+        const sb_csr &A = *(const sb_csr *)M.mat;
+        return !A.plan || A.plan->kernel != SB_CSR_MERGE;
+    }
+    return false;
+}
+
+template <class V, class I>
+sb_status cgs_solve(const SolveArgs &a) {
+    sb_error *err = a.err;
+    int64_t n = 0;
+    sb_status s = check_solve_args<V>(a, n);
+    if (s != SB_OK) return s;
+    const int64_t cap = a.log->history_cap;
+    SolverWs w = carve_ws(a.ws, SB_SOLVER_CGS, sizeof(V), n, 0, cap);
+    V *r = ws_vec<V>(w, 0), *rs = ws_vec<V>(w, 1), *u = ws_vec<V>(w, 2), *p = ws_vec<V>(w, 3),
+      *q = ws_vec<V>(w, 4), *v = ws_vec<V>(w, 5), *uh = ws_vec<V>(w, 6), *ph = ws_vec<V>(w, 7),
+      *t = ws_vec<V>(w, 8);
+    const V *b = (const V *)a.b->data, *inv = (const V *)a.inv;
+    V *x = (V *)a.x->data;
+    Ctl *ctl = w.ctl;
+    double *part = w.partials;
+    const sb_matrix M = *a.A;
+    const bool fused = row_owned_format(M);
+    Ctl h = initial_ctl(*a.crit, w, cap);
+    LoopSpec spec;
+    spec.key = "cgs" + std::to_string(sizeof(V)) + std::to_string(sizeof(I)) + "|" + matrix_key(M) +
+               ptr_key({a.inv, b, x, a.ws});
+    spec.poll_chunk = 8;
+    spec.setup = [=](cudaStream_t st) -> cudaError_t {
+        cudaError_t e = matrix_apply<V, I>(M, x, 1, t, 1, EpiStore<V>{t, 1}, st);
+        if (e != cudaSuccess) return e;
+        e = launch_ew<2>(n, ctl, part, ShadowInit<V>{{}, b, t, r, rs}, st);
+        if (e != cudaSuccess) return e;
+        // CGS keeps rho_prev = 0 until the first iteration ends (solvers.py:240)
+        return cudaSuccess;
+    };
+    spec.body = [=](cudaStream_t st) -> cudaError_t {
+        cudaError_t e = launch_ew<0>(n, ctl, part, CgsDirection<V>{{}, r, q, inv, u, p, ph, 0, false}, st);
+        if (e != cudaSuccess) return e;
+        e = matrix_apply<V, I>(M, ph, 1, v, 1, EpiSolver<V, 1, BiSigmaFin>{v, rs, nullptr, ctl, part, {}}, st);
+        if (e != cudaSuccess) return e;
+        e = launch_ew<0>(n, ctl, part, CgsQ<V>{{}, u, v, inv, q, uh, x, 0}, st);
+        if (e != cudaSuccess) return e;
+        if (fused) return matrix_apply<V, I>(M, uh, 1, t, 1, EpiCgsResidual<V>{t, r, rs, ctl, part}, st);
+        e = matrix_apply<V, I>(M, uh, 1, t, 1, EpiSolverStore<V, NeverSkip>{t, ctl, {}}, st);
+        if (e != cudaSuccess) return e;
+        return launch_ew<2>(n, ctl, part, CgsResidualPass<V>{{}, t, rs, r, 0}, st);
+    };
+    s = run_loop(spec, ctl, h, a.st, err);
+    if (s != SB_OK) return s;
+    return finish_log(h, a, w);
+}
+
+}  // namespace sb
+
+using namespace sb;
+
+extern "C" {
+
+#define SB_DEFS(V, VN, I, IN) \
+    sb_status sb_cgs_solve_##VN##_##IN(const sb_matrix *a, const void *inv_diag,                   \
+                                       const sb_dense *b, sb_dense *x, const sb_criteria *crit,    \
+                                       void *workspace, sb_log *log, sb_stream_t stream,           \
+                                       sb_error *err) {                                            \
+        SB_GUARD_BEGIN                                                                             \
+        return cgs_solve<V, I>(SolveArgs{a, inv_diag, b, x, crit, 0, workspace, log,               \
+                                         as_stream(stream), err});                                 \
+        SB_GUARD_END                                                                               \
+    }
+
+SB_DEFS(float, float, int32_t, i32)
+SB_DEFS(float, float, int64_t, i64)
+SB_DEFS(double, double, int32_t, i32)
+SB_DEFS(double, double, int64_t, i64)
+
+}  // extern "C"

@@ -1,0 +1,310 @@
+// gmres.cu -- restarted GMRES(m) on the device (solvers.py:322-399): single-pass MGS with fused
+// dots, Givens rotations and criteria in the reductions' last block, one graph per cycle.
+#include <cmath>
+
+#include "solver_common.cuh"
+
+namespace sb {
+
+// ================================================================ GMRES(m) (solvers.py:322-399)
+struct SkipCycleEnd {
+    __device__ __forceinline__ bool skip(const Ctl *c) const { return c->cycle_end != 0; }
+    __device__ __forceinline__ void prepare(const Ctl *) {}
+};
+struct SkipUnlessCycleEnd {
+    __device__ __forceinline__ bool skip(const Ctl *c) const { return c->cycle_end == 0; }
+    __device__ __forceinline__ void prepare(const Ctl *) {}
+};
+
+// restart: r = b - A x, beta = ||r||; reset the cycle's small dense state
+template <class V>
+struct GmRestart : SkipNone {
+    const V *b, *t;
+    V *r;
+    __device__ __forceinline__ void elem(int64_t i, double (&part)[1]) const {
+        const V ri = axpy_e(-1.0, t[i], b[i]);
+        r[i] = ri;
+        part[0] = addd(part[0], mulp(ri, ri));
+    }
+    __device__ __forceinline__ void last(Ctl *c, const double (&tot)[1]) const {
+        const double beta = sqrt(tot[0]);
+        if (beta == 0.0) {
+            if (c->iter == 0) exact_log(c);
+            else finish_with(c, c->iter, STOP_RESIDUAL);
+            return;
+        }
+        const int64_t m = c->dim;
+        c->beta_restart = beta;
+        for (int64_t i = 0; i <= m; ++i) c->g[i] = 0.0;
+        for (int64_t i = 0; i < m; ++i) c->cs[i] = c->sn[i] = 0.0;
+        for (int64_t i = 0; i < m * m; ++i) c->R[i] = 0.0;
+        c->g[0] = beta;
+        c->j = 0;
+        c->cycle_end = 0;
+        c->finish = 0;
+        c->cycle += 1;
+    }
+};
+
+// v0 = (1 / beta) r  (copy + scal(1.0 / beta))
+template <class V>
+struct GmFirstBasis : SkipNone {
+    const V *r;
+    V *v0;
+    double inv_beta;
+    __device__ __forceinline__ void prepare(const Ctl *c) { inv_beta = 1.0 / c->beta_restart; }
+    __device__ __forceinline__ void elem(int64_t i, double (&)[1]) const { v0[i] = scal_e(inv_beta, r[i]); }
+};
+
+// z = M v_j
+template <class V>
+struct GmPrecond : SkipCycleEnd {
+    const V *vj, *inv;
+    V *z;
+    __device__ __forceinline__ void elem(int64_t i, double (&)[1]) const { z[i] = vmul(vj[i], inv[i]); }
+};
+
+// w = A z with h_0j = v_0.w fused
+struct GmH0Fin {
+    __device__ __forceinline__ bool skip(const Ctl *c) const { return c->cycle_end != 0; }
+    __device__ __forceinline__ void last(Ctl *c, const double (&tot)[1]) const { c->hcol[0] = tot[0]; }
+};
+
+// one MGS step: w -= h_i v_i, then h_{i+1} = v_{i+1}.w (single pass)
+template <class V>
+struct GmMgsStep : SkipCycleEnd {
+    const V *vi, *vnext;
+    V *w;
+    int i;
+    double h;
+    __device__ __forceinline__ void prepare(const Ctl *c) { h = c->hcol[i]; }
+    __device__ __forceinline__ void elem(int64_t e, double (&part)[1]) const {
+        const V we = axpy_e(-h, vi[e], w[e]);
+        w[e] = we;
+        part[0] = addd(part[0], mulp(vnext[e], we));
+    }
+    __device__ __forceinline__ void last(Ctl *c, const double (&tot)[1]) const { c->hcol[i + 1] = tot[0]; }
+};
+
+// givens_rotation (solvers.py:138-143)
+__device__ __forceinline__ void givens(double a, double b, double &c, double &s, double &r) {
+    if (a == 0.0 && b == 0.0) {
+        c = 1.0;
+        s = 0.0;
+        r = 0.0;
+        return;
+    }
+    r = hypot(a, b);
+    c = __ddiv_rn(a, r);
+    s = __ddiv_rn(b, r);
+}
+
+// last MGS step of column j: w -= h_jj v_j, ||w||, then the reference's per-inner-iteration
+// scalar work: rotations, estimate |g_{j+1}|, criteria, happy breakdown, cycle end
+template <class V>
+struct GmMgsLast : SkipCycleEnd {
+    const V *vj;
+    V *w;
+    int j;
+    double h;
+    __device__ __forceinline__ void prepare(const Ctl *c) { h = c->hcol[j]; }
+    __device__ __forceinline__ void elem(int64_t e, double (&part)[1]) const {
+        const V we = axpy_e(-h, vj[e], w[e]);
+        w[e] = we;
+        part[0] = addd(part[0], mulp(we, we));
+    }
+    __device__ __forceinline__ void last(Ctl *c, const double (&tot)[1]) const {
+        double *hc = c->hcol;
+        const double hnorm = sqrt(tot[0]);
+        hc[j + 1] = hnorm;
+        for (int i = 0; i <= j + 1; ++i)
+            if (!isfinite(hc[i])) {
+                c->status = ST_NUMERIC;
+                c->status_iter = c->iter + 1;
+                stop_loop(c);
+                return;
+            }
+        for (int i = 0; i < j; ++i) {
+            const double hi = hc[i], hi1 = hc[i + 1];
+            hc[i] = __dadd_rn(__dmul_rn(c->cs[i], hi), __dmul_rn(c->sn[i], hi1));
+            hc[i + 1] = __dadd_rn(__dmul_rn(-c->sn[i], hi), __dmul_rn(c->cs[i], hi1));
+        }
+        double cr, sr, rr;
+        givens(hc[j], hc[j + 1], cr, sr, rr);
+        c->cs[j] = cr;
+        c->sn[j] = sr;
+        hc[j] = rr;
+        const int64_t m = c->dim;
+        for (int i = 0; i <= j; ++i) c->R[i * m + j] = hc[i];
+        c->g[j + 1] = __dmul_rn(-sr, c->g[j]);
+        c->g[j] = __dmul_rn(cr, c->g[j]);
+        const double est = fabs(c->g[j + 1]);
+        if (!isfinite(est)) {
+            c->status = ST_NUMERIC;
+            c->status_iter = c->iter + 1;
+            stop_loop(c);
+            return;
+        }
+        const int64_t total = c->iter + 1;
+        c->iter = total;
+        record(c, total, est);
+        const int reason = check_criteria(c, total, est, c->bnorm);
+        const bool happy = hnorm <= __dmul_rn(1e-30, c->bnorm);
+        c->hnorm = hnorm;
+        if (reason != STOP_NONE || happy || j + 1 == m) {
+            c->cycle_end = 1;
+            c->k = j + 1;
+            c->finish = reason != STOP_NONE;
+            c->stop_reason = reason;
+        } else {
+            c->j = j + 1;
+        }
+    }
+};
+
+// v_{j+1} = (1 / ||w||) w
+template <class V>
+struct GmNextBasis : SkipCycleEnd {
+    const V *w;
+    V *vn;
+    double inv_h;
+    __device__ __forceinline__ void prepare(const Ctl *c) { inv_h = 1.0 / c->hnorm; }
+    __device__ __forceinline__ void elem(int64_t e, double (&)[1]) const { vn[e] = scal_e(inv_h, w[e]); }
+};
+
+// _back_substitute (solvers.py:301-308)
+struct GmBackSub {
+    __device__ __forceinline__ bool skip(const Ctl *c) const { return c->cycle_end == 0; }
+    __device__ __forceinline__ void run(Ctl *c) const {
+        const int k = c->k;
+        const int64_t m = c->dim;
+        for (int i = k - 1; i >= 0; --i) {
+            double acc = c->g[i];
+            for (int q = i + 1; q < k; ++q) acc = __dsub_rn(acc, __dmul_rn(c->R[i * m + q], c->y[q]));
+            c->y[i] = __ddiv_rn(acc, c->R[i * m + i]);
+        }
+    }
+};
+
+// _gmres_update: zacc = sum_i axpy(y_i, v_i, zacc) (sequential, rounded per step);
+// x += M zacc; then finish if a criterion fired
+template <class V, int MAXK>
+struct GmUpdate : SkipUnlessCycleEnd {
+    const V *basis;
+    size_t vstride;  // elements between consecutive basis vectors
+    const V *inv;
+    V *x;
+    const double *y;
+    int k;
+    __device__ __forceinline__ void prepare(const Ctl *c) {
+        k = c->k;
+        y = c->y;
+    }
+    __device__ __forceinline__ void elem(int64_t e, double (&part)[1]) const {
+        V acc = (V)0;
+        for (int i = 0; i < k; ++i) acc = axpy_e(y[i], basis[(size_t)i * vstride + e], acc);
+        x[e] = axpy_e(1.0, precond_e(inv, e, acc), x[e]);
+        (void)part;
+    }
+    __device__ __forceinline__ void last(Ctl *c, const double (&)[1]) const {
+        if (c->finish) finish_with(c, c->iter, c->stop_reason);
+    }
+};
+
+template <class V, class I>
+sb_status gmres_solve(const SolveArgs &a) {
+    sb_error *err = a.err;
+    int64_t n = 0;
+    sb_status s = check_solve_args<V>(a, n);
+    if (s != SB_OK) return s;
+    const int64_t m = a.dim;
+    if (m < 1) return fail(err, SB_ERR_INVALID_ARGUMENT, "krylov_dim must be positive");
+    if (m > 4096) return fail(err, SB_ERR_UNSUPPORTED, "krylov_dim > 4096");
+    const int64_t cap = a.log->history_cap;
+    SolverWs w = carve_ws(a.ws, SB_SOLVER_GMRES, sizeof(V), n, m, cap);
+    V *basis = ws_vec<V>(w, 0);
+    const size_t vstride = w.vec_bytes / sizeof(V);
+    V *r = ws_vec<V>(w, (int)m + 1), *t = ws_vec<V>(w, (int)m + 2), *z = ws_vec<V>(w, (int)m + 3),
+      *wv = ws_vec<V>(w, (int)m + 4);
+    auto V_ = [=](int64_t i) { return basis + (size_t)i * vstride; };
+    const V *b = (const V *)a.b->data, *inv = (const V *)a.inv;
+    V *x = (V *)a.x->data;
+    Ctl *ctl = w.ctl;
+    double *part = w.partials;
+    const sb_matrix M = *a.A;
+    Ctl h = initial_ctl(*a.crit, w, cap);
+    h.dim = m;
+    double *sm = w.small;
+    h.hcol = sm;
+    h.g = sm + (m + 2);
+    h.cs = sm + 2 * (m + 2);
+    h.sn = sm + 3 * (m + 2);
+    h.y = sm + 4 * (m + 2);
+    h.R = sm + 4 * (m + 2) + m;
+    LoopSpec spec;
+    spec.key = "gmres" + std::to_string(sizeof(V)) + std::to_string(sizeof(I)) + "|" + std::to_string(m) +
+               "|" + matrix_key(M) + ptr_key({a.inv, b, x, a.ws});
+    spec.poll_chunk = 1;
+    spec.setup = [=](cudaStream_t st) -> cudaError_t {
+        return launch_ew<1>(n, ctl, part, NormB<V>{{}, b}, st);
+    };
+    spec.body = [=](cudaStream_t st) -> cudaError_t {
+        cudaError_t e = matrix_apply<V, I>(M, x, 1, t, 1, EpiSolverStore<V, NeverSkip>{t, ctl, {}}, st);
+        if (e != cudaSuccess) return e;
+        e = launch_ew<1>(n, ctl, part, GmRestart<V>{{}, b, t, r}, st);
+        if (e != cudaSuccess) return e;
+        e = launch_ew<0>(n, ctl, part, GmFirstBasis<V>{{}, r, V_(0), 0.0}, st);
+        if (e != cudaSuccess) return e;
+        for (int64_t j = 0; j < m; ++j) {
+            const V *zin = V_(j);
+            if (inv) {
+                e = launch_ew<0>(n, ctl, part, GmPrecond<V>{{}, V_(j), inv, z}, st);
+                if (e != cudaSuccess) return e;
+                zin = z;
+            }
+            e = matrix_apply<V, I>(M, zin, 1, wv, 1, EpiSolver<V, 1, GmH0Fin>{wv, V_(0), nullptr, ctl, part, {}}, st);
+            if (e != cudaSuccess) return e;
+            for (int64_t i = 0; i < j; ++i) {
+                e = launch_ew<1>(n, ctl, part, GmMgsStep<V>{{}, V_(i), V_(i + 1), wv, (int)i, 0.0}, st);
+                if (e != cudaSuccess) return e;
+            }
+            e = launch_ew<1>(n, ctl, part, GmMgsLast<V>{{}, V_(j), wv, (int)j, 0.0}, st);
+            if (e != cudaSuccess) return e;
+            if (j + 1 < m) {
+                e = launch_ew<0>(n, ctl, part, GmNextBasis<V>{{}, wv, V_(j + 1), 0.0}, st);
+                if (e != cudaSuccess) return e;
+            }
+        }
+        scalar_kernel<<<1, 1, 0, st>>>(ctl, GmBackSub{});
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        return launch_ew<1>(n, ctl, part, GmUpdate<V, 0>{{}, basis, vstride, inv, x, nullptr, 0}, st);
+    };
+    s = run_loop(spec, ctl, h, a.st, err);
+    if (s != SB_OK) return s;
+    return finish_log(h, a, w);
+}
+
+}  // namespace sb
+
+using namespace sb;
+
+extern "C" {
+
+#define SB_DEFS(V, VN, I, IN) \
+    sb_status sb_gmres_solve_##VN##_##IN(const sb_matrix *a, const void *inv_diag,                 \
+                                         const sb_dense *b, sb_dense *x, const sb_criteria *crit,  \
+                                         int64_t krylov_dim, void *workspace, sb_log *log,         \
+                                         sb_stream_t stream, sb_error *err) {                      \
+        SB_GUARD_BEGIN                                                                             \
+        return gmres_solve<V, I>(SolveArgs{a, inv_diag, b, x, crit, krylov_dim, workspace, log,    \
+                                           as_stream(stream), err});                               \
+        SB_GUARD_END                                                                               \
+    }
+
+SB_DEFS(float, float, int32_t, i32)
+SB_DEFS(float, float, int64_t, i64)
+SB_DEFS(double, double, int32_t, i32)
+SB_DEFS(double, double, int64_t, i64)
+
+}  // extern "C"

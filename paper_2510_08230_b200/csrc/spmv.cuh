@@ -1,0 +1,594 @@
+// spmv.cuh -- sm_100a SpMV kernels for CSR / COO / ELL / SELL-P / Hybrid.
+//
+// Reference semantics: linop.spmv_csr / spmv_coo (linop.py:102-159) ->
+// _kernels.spmv_csr_rows / spmv_coo_entries (_kernels.py:62-88): x[i] is the fp64
+// sum of the row's products, written with one rounding to the value type; rows with
+// no entries write 0.
+//
+// Kernels that own whole rows (strict, stream, vector, ELL, SELL-P) take an
+// epilogue `Epi` that receives (row, fp64 sum): the plain store, or a solver
+// epilogue that also accumulates a fused dot product (e.g. CG's p.Ap) and finalises
+// it with a deterministic grid reduction.  Row-splitting kernels (merge-path CSR,
+// segmented COO) write x and are followed by a carry fix-up pass.
+//
+// Row-accumulation order:
+//   strict / stream / ELL / SELL-P: sequential in stored order -> bitwise equal to
+//     the reference for every value type (the stream kernel is the production path
+//     for regular matrices such as the Poisson configs);
+//   vector / merge / COO: per-lane or per-thread sequential partials combined by a
+//     fixed tree -> deterministic, within the 1e-12 / 1e-5 scale tolerance.
+#pragma once
+
+#include "common.cuh"
+
+namespace sb {
+
+// ============================================================ epilogues
+template <class V>
+struct EpiStore {
+    static constexpr int N = 1;  // no reduction; N=1 only sizes the (unused) partial array
+    V *x;
+    int64_t ldx;
+    __device__ __forceinline__ bool skip() const { return false; }
+    __device__ __forceinline__ void row(int64_t i, double acc, double (&)[N]) const {
+        x[i * ldx] = (V)acc;
+    }
+    __device__ __forceinline__ void finish(double (&)[N]) const {}
+};
+
+// ============================================================ CSR: strict (device oracle)
+// One thread per row straight from global memory: the reference loop verbatim.
+template <class V, class I, class Epi>
+__global__ void __launch_bounds__(256) csr_strict_kernel(int64_t rows, const I *__restrict__ rp,
+                                                         const I *__restrict__ ci,
+                                                         const V *__restrict__ val,
+                                                         const V *__restrict__ b, int64_t ldb,
+                                                         Epi epi) {
+    if (epi.skip()) return;
+    double part[Epi::N] = {};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int64_t k = rp[i]; k < (int64_t)rp[i + 1]; ++k)
+            acc = addd(acc, mulp(val[k], __ldg(b + (int64_t)ci[k] * ldb)));
+        epi.row(i, acc, part);
+    }
+    epi.finish(part);
+}
+
+// ============================================================ CSR: stream (TMA-staged)
+// Persistent CTAs walk fixed blocks of R rows.  For each block one elected thread
+// issues 1-D TMA bulk copies (cp.async.bulk, completion on an mbarrier) of the
+// block's row_ptrs slice and its contiguous value / column ranges into a two-stage
+// shared-memory ring, prefetching block k+1 while block k is consumed.  Each thread
+// then reduces one row sequentially from shared memory (gathering b through L1/L2),
+// which reproduces the reference's accumulation order exactly.
+template <class V, class I>
+struct StreamLayout {
+    static constexpr int VV = 16 / sizeof(V);
+    static constexpr int VI = 16 / sizeof(I);
+    int cap_v, cap_c, cap_r;  // elements per stage
+    __host__ __device__ StreamLayout(int R, int nnz_cap) {
+        cap_v = (nnz_cap + 2 * VV + 3) & ~3;
+        cap_c = (nnz_cap + 2 * VI + 3) & ~3;
+        cap_r = (R + 1 + 2 * VI + 3) & ~3;
+    }
+    __host__ __device__ size_t stage_bytes() const {
+        size_t b = (size_t)cap_v * sizeof(V);
+        b = (b + 15) & ~size_t(15);
+        b += (size_t)cap_c * sizeof(I);
+        b = (b + 15) & ~size_t(15);
+        b += (size_t)cap_r * sizeof(I);
+        return (b + 15) & ~size_t(15);
+    }
+    __host__ __device__ size_t off_c() const { return ((size_t)cap_v * sizeof(V) + 15) & ~size_t(15); }
+    __host__ __device__ size_t off_r() const {
+        return (off_c() + (size_t)cap_c * sizeof(I) + 15) & ~size_t(15);
+    }
+};
+
+struct StreamMeta {
+    int64_t r0, r1, av, ac, ar;  // block rows [r0, r1); smem bases (global element index of slot 0)
+};
+
+template <class T>
+__device__ __forceinline__ uint32_t stage_range(const T *g, int64_t lo, int64_t hi, int64_t len,
+                                                T *s, int64_t &base) {
+    // copy g[lo, hi) (hi <= len) into s, starting at the 16-byte aligned element `base`;
+    // returns the bulk bytes issued (the unaligned tail beyond len's last full vector is
+    // copied with scalar loads).
+    constexpr int VE = 16 / sizeof(T);
+    base = lo & ~(int64_t)(VE - 1);
+    const int64_t full_end = len & ~(int64_t)(VE - 1);
+    int64_t bulk_end = (hi + VE - 1) & ~(int64_t)(VE - 1);
+    if (bulk_end > full_end) bulk_end = full_end;
+    if (bulk_end < base) bulk_end = base;
+    for (int64_t e = bulk_end; e < hi; ++e) s[e - base] = g[e];
+    return (uint32_t)((bulk_end - base) * (int64_t)sizeof(T));
+}
+
+template <class V, class I, int R, class Epi>
+__global__ void __launch_bounds__(R) csr_stream_kernel(int64_t rows, int64_t nnz,
+                                                       const I *__restrict__ rp,
+                                                       const I *__restrict__ ci,
+                                                       const V *__restrict__ val,
+                                                       const V *__restrict__ b, int64_t ldb,
+                                                       int nnz_cap, Epi epi) {
+    if (epi.skip()) return;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ StreamMeta meta[2];
+    const StreamLayout<V, I> L(R, nnz_cap);
+    const size_t sb = L.stage_bytes();
+    const int tid = threadIdx.x;
+    const int64_t nblk = (rows + R - 1) / R;
+    const uint64_t pol = policy_evict_first();
+
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    auto issue = [&](int64_t blk, int s) {  // thread 0 only
+        unsigned char *st = smem + s * sb;
+        V *sv = reinterpret_cast<V *>(st);
+        I *sc = reinterpret_cast<I *>(st + L.off_c());
+        I *sr = reinterpret_cast<I *>(st + L.off_r());
+        const int64_t r0 = blk * R, r1 = r0 + R < rows ? r0 + R : rows;
+        const int64_t k0 = rp[r0], k1 = rp[r1];
+        StreamMeta m;
+        m.r0 = r0;
+        m.r1 = r1;
+        uint32_t bv = stage_range(val, k0, k1, nnz, sv, m.av);
+        uint32_t bc = stage_range(ci, k0, k1, nnz, sc, m.ac);
+        uint32_t br = stage_range(rp, r0, r1 + 1, rows + 1, sr, m.ar);
+        meta[s] = m;
+        mbar_arrive_expect_tx(&bar[s], bv + bc + br);
+        if (bv) bulk_g2s(sv, val + m.av, bv, &bar[s], pol);
+        if (bc) bulk_g2s(sc, ci + m.ac, bc, &bar[s], pol);
+        if (br) bulk_g2s(sr, rp + m.ar, br, &bar[s], pol);
+    };
+
+    double part[Epi::N] = {};
+    int64_t blk = blockIdx.x;
+    if (tid == 0 && blk < nblk) issue(blk, 0);
+    for (int it = 0; blk < nblk; blk += gridDim.x, ++it) {
+        const int s = it & 1;
+        const uint32_t parity = (it >> 1) & 1;
+        if (tid == 0 && blk + gridDim.x < nblk) issue(blk + gridDim.x, s ^ 1);
+        mbar_wait(&bar[s], parity);
+        const unsigned char *st = smem + s * sb;
+        const V *sv = reinterpret_cast<const V *>(st);
+        const I *sc = reinterpret_cast<const I *>(st + L.off_c());
+        const I *sr = reinterpret_cast<const I *>(st + L.off_r());
+        const StreamMeta m = meta[s];
+        const int64_t i = m.r0 + tid;
+        if (i < m.r1) {
+            const int64_t kb = sr[i - m.ar], ke = sr[i + 1 - m.ar];
+            double acc = 0.0;
+            int64_t k = kb;
+            for (; k + 8 <= ke; k += 8) {
+                V vv[8], bb[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    vv[j] = sv[k + j - m.av];
+                    bb[j] = __ldg(b + (int64_t)sc[k + j - m.ac] * ldb);
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc = addd(acc, mulp(vv[j], bb[j]));
+            }
+            if (k < ke) {
+                V vv[8], bb[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (k + j < ke) {
+                        vv[j] = sv[k + j - m.av];
+                        bb[j] = __ldg(b + (int64_t)sc[k + j - m.ac] * ldb);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (k + j < ke) acc = addd(acc, mulp(vv[j], bb[j]));
+            }
+            epi.row(i, acc, part);
+        }
+        __syncthreads();  // stage s fully consumed before it is re-issued
+    }
+    epi.finish(part);
+}
+
+// ============================================================ CSR: vector (sub-warp per row)
+// S lanes per row (S in 2..32 chosen from the mean row length), strided partials,
+// fixed shuffle tree.
+template <class V, class I, int S, class Epi>
+__global__ void __launch_bounds__(256) csr_vector_kernel(int64_t rows, const I *__restrict__ rp,
+                                                         const I *__restrict__ ci,
+                                                         const V *__restrict__ val,
+                                                         const V *__restrict__ b, int64_t ldb,
+                                                         Epi epi) {
+    if (epi.skip()) return;
+    double part[Epi::N] = {};
+    const int lane = threadIdx.x % S;
+    const int64_t group = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / S;
+    const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / S;
+    const int64_t trips = (rows + ngroups - 1) / ngroups;  // uniform trip count keeps shuffles converged
+    for (int64_t t = 0; t < trips; ++t) {
+        const int64_t i = group + t * ngroups;
+        double acc = 0.0;
+        if (i < rows) {
+            const int64_t kb = rp[i], ke = rp[i + 1];
+            for (int64_t k = kb + lane; k < ke; k += S)
+                acc = addd(acc, mulp(ld_stream(val + k), __ldg(b + (int64_t)ld_stream(ci + k) * ldb)));
+        }
+#pragma unroll
+        for (int o = S / 2; o > 0; o >>= 1) acc = addd(acc, __shfl_down_sync(0xffffffffu, acc, o, S));
+        if (lane == 0 && i < rows) epi.row(i, acc, part);
+    }
+    epi.finish(part);
+}
+
+// ============================================================ reduce-by-key block scan
+// Inclusive scan of (key, value) pairs in thread order with
+//   (k1, v1) (+) (k2, v2) = (k2, k1 == k2 ? v1 + v2 : v2)
+// (keys are non-decreasing across threads).  Returns the inclusive pair in
+// (key, val) and the exclusive pair (the previous thread's inclusive pair) in
+// (ex_key, ex_val).  Fixed combination tree -> deterministic.
+template <int NT>
+__device__ __forceinline__ void scan_by_key(int64_t &key, double &val, int64_t &ex_key,
+                                            double &ex_val) {
+    static_assert(NT % 32 == 0 && NT <= 1024, "block size");
+    __shared__ int64_t s_k[NT / 32];
+    __shared__ double s_v[NT / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t k2 = __shfl_up_sync(0xffffffffu, key, o);
+        const double v2 = __shfl_up_sync(0xffffffffu, val, o);
+        if (lane >= o && k2 == key) val = addd(v2, val);
+    }
+    if (lane == 31) {
+        s_k[warp] = key;
+        s_v[warp] = val;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        int64_t wk = lane < NT / 32 ? s_k[lane] : INT64_MAX;
+        double wv = lane < NT / 32 ? s_v[lane] : 0.0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t k2 = __shfl_up_sync(0xffffffffu, wk, o);
+            const double v2 = __shfl_up_sync(0xffffffffu, wv, o);
+            if (lane >= o && k2 == wk) wv = addd(v2, wv);
+        }
+        if (lane < NT / 32) {
+            s_k[lane] = wk;
+            s_v[lane] = wv;
+        }
+    }
+    __syncthreads();
+    const int64_t pk = warp > 0 ? s_k[warp - 1] : INT64_MIN;
+    const double pv = warp > 0 ? s_v[warp - 1] : 0.0;
+    // keys are non-decreasing, so an equal key in the previous warps' aggregate means this
+    // thread's run started there (and its in-warp aggregate covers lanes 0..lane)
+    if (pk == key) val = addd(pv, val);
+    int64_t ek = __shfl_up_sync(0xffffffffu, key, 1);
+    double ev = __shfl_up_sync(0xffffffffu, val, 1);
+    if (lane == 0) {
+        ek = pk;
+        ev = pv;
+    }
+    ex_key = ek;
+    ex_val = ev;
+    __syncthreads();  // s_k / s_v reusable by the next call
+}
+
+// ============================================================ CSR: merge-path
+// Load-balanced: every tile owns exactly NT*IPT merge items (row ends + nonzeros),
+// so a CTA's work is independent of the row-length distribution.  Tile start
+// coordinates come from the plan (merge_path_partition_kernel).  Products are
+// staged in shared memory, each thread walks IPT items sequentially, partial rows
+// are joined by a block reduce-by-key scan, and a tile's unfinished last row is
+// handed to the carry fix-up kernel.
+template <class I>
+__device__ __forceinline__ int64_t merge_search(int64_t diag, const I *a, int64_t a_len, int64_t b0,
+                                                int64_t b_len) {
+    // CUB-style MergePathSearch of list a (row ends) against b = b0, b0+1, ...:
+    // the number of a-items consumed after `diag` merge steps.
+    int64_t lo = diag - b_len > 0 ? diag - b_len : 0;
+    int64_t hi = diag < a_len ? diag : a_len;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)a[mid] <= b0 + diag - mid - 1) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+template <class I>
+__global__ void merge_path_partition_kernel(int64_t rows, int64_t nnz, const I *__restrict__ rp,
+                                            int64_t items_per_tile, int64_t num_tiles,
+                                            int64_t *tile_rows, int64_t *tile_nnz) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t > num_tiles) return;
+    int64_t diag = t * items_per_tile;
+    if (diag > rows + nnz) diag = rows + nnz;
+    const int64_t x = merge_search(diag, rp + 1, rows, 0, nnz);
+    tile_rows[t] = x;
+    tile_nnz[t] = diag - x;
+}
+
+template <class V, class I, int NT, int IPT>
+__global__ void __launch_bounds__(NT) csr_merge_kernel(int64_t rows, const I *__restrict__ rp,
+                                                       const I *__restrict__ ci,
+                                                       const V *__restrict__ val,
+                                                       const V *__restrict__ b, int64_t ldb, V *x,
+                                                       int64_t ldx, const int64_t *tile_rows,
+                                                       const int64_t *tile_nnz, int64_t num_tiles,
+                                                       int64_t *carry_rows, double *carry_vals) {
+    constexpr int TILE = NT * IPT;
+    __shared__ I s_end[TILE + 1];
+    __shared__ double s_prod[TILE];
+    __shared__ double s_out[TILE];
+    for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int64_t row_s = tile_rows[tile], k_s = tile_nnz[tile];
+        const int64_t row_e = tile_rows[tile + 1], k_e = tile_nnz[tile + 1];
+        const int64_t nA = row_e - row_s, nB = k_e - k_s;
+        const int64_t nload = (row_e + 1 < rows ? row_e + 1 : rows) - row_s;  // ends of rows row_s..row_e
+        for (int64_t j = threadIdx.x; j < nload; j += NT) s_end[j] = rp[row_s + j + 1];
+        for (int64_t j = threadIdx.x; j < nB; j += NT) {
+            const int64_t k = k_s + j;
+            s_prod[j] = mulp(ld_stream(val + k), __ldg(b + (int64_t)ld_stream(ci + k) * ldb));
+        }
+        __syncthreads();
+        const int64_t total = nA + nB;
+        const int64_t d0 = (int64_t)threadIdx.x * IPT;
+        int64_t r = nA;
+        bool emitted = false;
+        int64_t first_row = -1;
+        double acc = 0.0;
+        if (d0 < total) {
+            r = merge_search(d0, s_end, nA, k_s, nB);
+            int64_t k = k_s + d0 - r;
+            for (int it = 0; it < IPT && d0 + it < total; ++it) {
+                if (r < nload && k < (int64_t)s_end[r]) {
+                    acc = addd(acc, s_prod[k - k_s]);
+                    ++k;
+                } else {
+                    s_out[r] = acc;
+                    if (!emitted) {
+                        emitted = true;
+                        first_row = r;
+                    }
+                    acc = 0.0;
+                    ++r;
+                }
+            }
+        }
+        int64_t key = r, ex_key;
+        double cv = acc, ex_val;
+        scan_by_key<NT>(key, cv, ex_key, ex_val);
+        if (emitted && ex_key == first_row) s_out[first_row] = addd(ex_val, s_out[first_row]);
+        __syncthreads();
+        for (int64_t j = threadIdx.x; j < nA; j += NT) x[(row_s + j) * ldx] = (V)s_out[j];
+        if (threadIdx.x == NT - 1) {
+            // inclusive total over the tile = this tile's partial of row row_e (idle threads
+            // carry key nA, so the scan propagates it to the last thread)
+            const int64_t consumed = nA > 0 ? k_e - (int64_t)s_end[nA - 1] : nB;
+            const bool carry = row_e < rows && consumed > 0;
+            carry_rows[tile] = carry ? row_e : -1;
+            carry_vals[tile] = carry ? cv : 0.0;
+        }
+        __syncthreads();
+    }
+}
+
+// Deterministic carry fix-up: runs of equal carry rows are summed in tile order and
+// added once to the row's value (written by the tile that finished the row).
+template <class V>
+__global__ void carry_fixup_kernel(int64_t num_tiles, const int64_t *carry_rows,
+                                   const double *carry_vals, V *x, int64_t ldx) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= num_tiles) return;
+    const int64_t r = carry_rows[t];
+    if (r < 0 || (t > 0 && carry_rows[t - 1] == r)) return;
+    double s = carry_vals[t];
+    for (int64_t u = t + 1; u < num_tiles && carry_rows[u] == r; ++u) s = addd(s, carry_vals[u]);
+    x[r * ldx] = (V)addd((double)x[r * ldx], s);
+}
+
+// ============================================================ COO: segmented reduction
+// Tiles of NT*IPT consecutive (sorted) entries.  Each thread reduces IPT entries by
+// row key; a block reduce-by-key scan joins runs crossing threads; runs finished in
+// the tile are written; a run continuing into the next tile is carried to the
+// fix-up kernel.  With accumulate == false the tile also zeroes the empty rows it
+// owns (gaps between its keys, plus the leading / trailing gaps in the first / last
+// tile), replacing the reference's separate zero pass (linop.py:155).  With
+// accumulate == true results are added into x (the Hybrid format's COO tail).
+template <class V, class I, int NT, int IPT>
+__global__ void __launch_bounds__(NT) coo_kernel(int64_t rows, int64_t nnz, const I *__restrict__ ri,
+                                                 const I *__restrict__ ci, const V *__restrict__ val,
+                                                 const V *__restrict__ b, int64_t ldb, V *x,
+                                                 int64_t ldx, int64_t num_tiles, int64_t *carry_rows,
+                                                 double *carry_vals, bool accumulate) {
+    constexpr int TILE = NT * IPT;
+    __shared__ double s_prod[TILE];
+    __shared__ int64_t s_key[TILE + 1];
+    for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int64_t e0 = tile * TILE;
+        const int64_t e1 = e0 + TILE < nnz ? e0 + TILE : nnz;
+        const int64_t ne = e1 - e0;
+        for (int64_t j = threadIdx.x; j < ne; j += NT) {
+            const int64_t e = e0 + j;
+            s_key[j] = (int64_t)ld_stream(ri + e);
+            s_prod[j] = mulp(ld_stream(val + e), __ldg(b + (int64_t)ld_stream(ci + e) * ldb));
+        }
+        if (threadIdx.x == 0) s_key[ne] = e1 < nnz ? (int64_t)ri[e1] : INT64_MAX;
+        __syncthreads();
+        if (!accumulate) {
+            const int64_t prev = e0 == 0 ? -1 : (int64_t)ri[e0 - 1];
+            for (int64_t j = threadIdx.x; j < ne; j += NT) {
+                const int64_t lo = (j == 0 ? prev : s_key[j - 1]) + 1, hi = s_key[j];
+                for (int64_t g = lo; g < hi; ++g) x[g * ldx] = (V)0;
+            }
+            if (tile == num_tiles - 1 && threadIdx.x == 0)
+                for (int64_t g = s_key[ne - 1] + 1; g < rows; ++g) x[g * ldx] = (V)0;
+        }
+        // pass 1: this thread's trailing run (carry-out)
+        const int64_t j0 = (int64_t)threadIdx.x * IPT;
+        const int64_t j1 = j0 + IPT < ne ? j0 + IPT : ne;
+        const bool active = j0 < ne;
+        int64_t key = active ? s_key[j0] : INT64_MAX;
+        double acc = 0.0;
+        for (int64_t j = j0; j < j1; ++j) {
+            if (s_key[j] != key) {
+                key = s_key[j];
+                acc = 0.0;
+            }
+            acc = addd(acc, s_prod[j]);
+        }
+        int64_t ex_key;
+        double cv = acc, ex_val;
+        scan_by_key<NT>(key, cv, ex_key, ex_val);
+        // pass 2: emit runs that finish inside this thread's range
+        if (active) {
+            int64_t k2 = s_key[j0];
+            double a2 = ex_key == k2 ? ex_val : 0.0;
+            for (int64_t j = j0; j < j1; ++j) {
+                if (s_key[j] != k2) {
+                    x[k2 * ldx] = accumulate ? (V)addd((double)x[k2 * ldx], a2) : (V)a2;
+                    k2 = s_key[j];
+                    a2 = 0.0;
+                }
+                a2 = addd(a2, s_prod[j]);
+            }
+            if (s_key[j1] != k2) x[k2 * ldx] = accumulate ? (V)addd((double)x[k2 * ldx], a2) : (V)a2;
+            if (j1 == ne) {
+                // last active thread: its inclusive pair is the tile's trailing run
+                const bool carry = s_key[ne] == k2;
+                carry_rows[tile] = carry ? k2 : -1;
+                carry_vals[tile] = carry ? cv : 0.0;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ============================================================ ELL (column-major)
+// RPT consecutive rows per thread with 16-byte vector loads of values (and 8/16-byte
+// loads of column indices); per-row order is the stored order -> bitwise = reference.
+template <class V, class I, int RPT, class Epi>
+__global__ void __launch_bounds__(256) ell_kernel(int64_t rows, int64_t width, int64_t stride,
+                                                  const I *__restrict__ col, const V *__restrict__ val,
+                                                  const V *__restrict__ b, int64_t ldb, Epi epi) {
+    if (epi.skip()) return;
+    double part[Epi::N] = {};
+    const int64_t groups = (rows + RPT - 1) / RPT;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < groups;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i0 = g * RPT;
+        double acc[RPT];
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) acc[r] = 0.0;
+        for (int64_t k = 0; k < width; ++k) {
+            const int64_t base = k * stride + i0;
+            V vv[RPT];
+            I cc[RPT];
+            if constexpr (RPT * sizeof(V) == 16) {
+                int4 raw = __ldcs(reinterpret_cast<const int4 *>(val + base));
+                memcpy(vv, &raw, 16);
+            } else {
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) vv[r] = __ldcs(val + base + r);
+            }
+            if constexpr (RPT * sizeof(I) == 16) {
+                int4 raw = __ldcs(reinterpret_cast<const int4 *>(col + base));
+                memcpy(cc, &raw, 16);
+            } else if constexpr (RPT * sizeof(I) == 8) {
+                int2 raw = __ldcs(reinterpret_cast<const int2 *>(col + base));
+                memcpy(cc, &raw, 8);
+            } else {
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) cc[r] = __ldcs(col + base + r);
+            }
+#pragma unroll
+            for (int r = 0; r < RPT; ++r)
+                if (cc[r] >= 0) acc[r] = addd(acc[r], mulp(vv[r], __ldg(b + (int64_t)cc[r] * ldb)));
+        }
+#pragma unroll
+        for (int r = 0; r < RPT; ++r)
+            if (i0 + r < rows) epi.row(i0 + r, acc[r], part);
+    }
+    epi.finish(part);
+}
+
+// ============================================================ SELL-P
+// Slices of S rows; entry k of row i (slice s) at (slice_sets[s] + k)*S + i%S.
+// RPT consecutive rows of one slice per thread (S % RPT == 0), vector loads.
+template <class V, class I, int RPT, class Epi>
+__global__ void __launch_bounds__(256) sellp_kernel(int64_t rows, int64_t S,
+                                                    const I *__restrict__ slice_lengths,
+                                                    const I *__restrict__ slice_sets,
+                                                    const I *__restrict__ col,
+                                                    const V *__restrict__ val,
+                                                    const V *__restrict__ b, int64_t ldb, Epi epi) {
+    if (epi.skip()) return;
+    double part[Epi::N] = {};
+    const int64_t nslices = (rows + S - 1) / S;
+    const int64_t groups = nslices * (S / RPT);
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < groups;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i0 = g * RPT;
+        const int64_t s = i0 / S, l0 = i0 % S;
+        const int64_t len = slice_lengths[s];
+        const int64_t off = (int64_t)slice_sets[s] * S + l0;
+        double acc[RPT];
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) acc[r] = 0.0;
+        for (int64_t k = 0; k < len; ++k) {
+            const int64_t base = off + k * S;
+            V vv[RPT];
+            I cc[RPT];
+            if constexpr (RPT * sizeof(V) == 16) {
+                int4 raw = __ldcs(reinterpret_cast<const int4 *>(val + base));
+                memcpy(vv, &raw, 16);
+            } else {
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) vv[r] = __ldcs(val + base + r);
+            }
+            if constexpr (RPT * sizeof(I) == 16) {
+                int4 raw = __ldcs(reinterpret_cast<const int4 *>(col + base));
+                memcpy(cc, &raw, 16);
+            } else if constexpr (RPT * sizeof(I) == 8) {
+                int2 raw = __ldcs(reinterpret_cast<const int2 *>(col + base));
+                memcpy(cc, &raw, 8);
+            } else {
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) cc[r] = __ldcs(col + base + r);
+            }
+#pragma unroll
+            for (int r = 0; r < RPT; ++r)
+                if (cc[r] >= 0) acc[r] = addd(acc[r], mulp(vv[r], __ldg(b + (int64_t)cc[r] * ldb)));
+        }
+#pragma unroll
+        for (int r = 0; r < RPT; ++r)
+            if (i0 + r < rows) epi.row(i0 + r, acc[r], part);
+    }
+    epi.finish(part);
+}
+
+// Row-owned epilogue applied after a row-splitting SpMV (merge / COO / Hybrid):
+// re-reads x and feeds it to the epilogue (so fused dots work for every format).
+template <class V, class Epi>
+__global__ void __launch_bounds__(256) epilogue_pass_kernel(int64_t rows, const V *x, int64_t ldx,
+                                                            Epi epi) {
+    if (epi.skip()) return;
+    double part[Epi::N] = {};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows;
+         i += (int64_t)gridDim.x * blockDim.x)
+        epi.row(i, (double)x[i * ldx], part);
+    epi.finish(part);
+}
+
+}  // namespace sb

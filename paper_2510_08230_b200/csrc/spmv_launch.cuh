@@ -1,0 +1,293 @@
+// spmv_launch.cuh -- host-side dispatch of the SpMV kernels for every storage format,
+// templated on the fused epilogue so the solvers reuse the same launchers.
+#pragma once
+
+#include "../../include/sparseb200.h"
+#include "spmv.cuh"
+
+namespace sb {
+
+template <class E>
+struct is_plain_store : std::false_type {};
+template <class V>
+struct is_plain_store<EpiStore<V>> : std::true_type {};
+
+// persistent-grid size for a kernel instantiation (cached per instantiation)
+template <class K>
+int persistent_grid(K kernel, int threads, size_t smem) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+    if (per_sm < 1) per_sm = 1;
+    return per_sm * device_info().sms;
+}
+
+constexpr int kMergeNT = 128, kMergeIPT = 8;      // 1024 merge items per tile
+constexpr int kCooNT = 128, kCooIPT = 8;          // 1024 entries per tile
+constexpr int kElemThreads = 256;
+
+inline int elem_grid(int64_t work_items) {
+    int64_t g = ceil_div(work_items, kElemThreads);
+    int64_t cap = (int64_t)device_info().sms * 8;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+// ---------------------------------------------------------------- CSR
+template <class V, class I, int R, class Epi>
+cudaError_t launch_csr_stream(const sb_csr &A, const V *b, int64_t ldb, const Epi &epi,
+                              cudaStream_t st) {
+    const int cap = A.plan->nnz_cap;
+    const StreamLayout<V, I> L(R, cap);
+    const size_t smem = 2 * L.stage_bytes();
+    static int configured = 0;
+    static int grid_per_smem[4] = {0, 0, 0, 0};
+    auto kern = csr_stream_kernel<V, I, R, Epi>;
+    if (!configured) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        configured = 1;
+    }
+    (void)grid_per_smem;
+    int grid = persistent_grid(kern, R, smem);
+    const int64_t nblk = ceil_div(A.rows, R);
+    if (grid > nblk) grid = (int)nblk;
+    kern<<<grid, R, smem, st>>>(A.rows, A.nnz, (const I *)A.row_ptrs, (const I *)A.col_idxs,
+                                (const V *)A.values, b, ldb, cap, epi);
+    return cudaGetLastError();
+}
+
+template <class V, class I, int S, class Epi>
+cudaError_t launch_csr_vector(const sb_csr &A, const V *b, int64_t ldb, const Epi &epi,
+                              cudaStream_t st) {
+    auto kern = csr_vector_kernel<V, I, S, Epi>;
+    int grid = persistent_grid(kern, 256, 0);
+    const int64_t need = ceil_div(A.rows * S, 256);
+    if (grid > need) grid = (int)(need > 0 ? need : 1);
+    kern<<<grid, 256, 0, st>>>(A.rows, (const I *)A.row_ptrs, (const I *)A.col_idxs,
+                               (const V *)A.values, b, ldb, epi);
+    return cudaGetLastError();
+}
+
+template <class V, class I, class Epi>
+cudaError_t launch_epilogue_pass(int64_t rows, const V *x, int64_t ldx, const Epi &epi,
+                                 cudaStream_t st) {
+    auto kern = epilogue_pass_kernel<V, Epi>;
+    int grid = persistent_grid(kern, 256, 0);
+    const int64_t need = ceil_div(rows, 256);
+    if (grid > need) grid = (int)(need > 0 ? need : 1);
+    kern<<<grid, 256, 0, st>>>(rows, x, ldx, epi);
+    return cudaGetLastError();
+}
+
+// x written by a row-splitting kernel: carry fix-up then (for fused epilogues) a pass
+template <class V>
+cudaError_t launch_fixup(int64_t num_tiles, const int64_t *carry_rows, const double *carry_vals,
+                         V *x, int64_t ldx, cudaStream_t st) {
+    if (num_tiles <= 0) return cudaSuccess;
+    carry_fixup_kernel<V><<<(int)ceil_div(num_tiles, 256), 256, 0, st>>>(num_tiles, carry_rows,
+                                                                          carry_vals, x, ldx);
+    return cudaGetLastError();
+}
+
+template <class V, class I>
+cudaError_t launch_csr_merge(const sb_csr &A, const V *b, int64_t ldb, V *x, int64_t ldx,
+                             cudaStream_t st) {
+    const sb_csr_plan &P = *A.plan;
+    auto kern = csr_merge_kernel<V, I, kMergeNT, kMergeIPT>;
+    int grid = persistent_grid(kern, kMergeNT, 0);
+    if (grid > P.num_tiles) grid = (int)P.num_tiles;
+    if (grid < 1) return cudaSuccess;
+    kern<<<grid, kMergeNT, 0, st>>>(A.rows, (const I *)A.row_ptrs, (const I *)A.col_idxs,
+                                    (const V *)A.values, b, ldb, x, ldx,
+                                    (const int64_t *)P.tile_rows, (const int64_t *)P.tile_nnz,
+                                    P.num_tiles, (int64_t *)P.carry_rows, (double *)P.carry_vals);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return launch_fixup<V>(P.num_tiles, (const int64_t *)P.carry_rows,
+                           (const double *)P.carry_vals, x, ldx, st);
+}
+
+template <class V>
+__global__ void fill_kernel(int64_t rows, int64_t cols, V *x, int64_t ldx, V v) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rows * cols;
+         t += (int64_t)gridDim.x * blockDim.x)
+        x[(t / cols) * ldx + t % cols] = v;
+}
+
+template <class V>
+cudaError_t launch_fill(int64_t rows, int64_t cols, V *x, int64_t ldx, V v, cudaStream_t st) {
+    if (rows * cols == 0) return cudaSuccess;
+    fill_kernel<V><<<elem_grid(rows * cols), kElemThreads, 0, st>>>(rows, cols, x, ldx, v);
+    return cudaGetLastError();
+}
+
+// x_out: where the raw SpMV result goes when the epilogue is not a plain store (the
+// solvers always pass their output vector here as well).
+template <class V, class I, class Epi>
+cudaError_t csr_apply(const sb_csr &A, const V *b, int64_t ldb, V *x_out, int64_t ldx,
+                      const Epi &epi, cudaStream_t st) {
+    const sb_csr_plan *P = A.plan;
+    int kernel = P ? P->kernel : SB_CSR_STRICT;
+    if (A.rows == 0) return cudaSuccess;
+    if (kernel == SB_CSR_STREAM) {
+        if (P->block_rows == 256) return launch_csr_stream<V, I, 256>(A, b, ldb, epi, st);
+        if (P->block_rows == 128) return launch_csr_stream<V, I, 128>(A, b, ldb, epi, st);
+        return launch_csr_stream<V, I, 64>(A, b, ldb, epi, st);
+    }
+    if (kernel == SB_CSR_VECTOR) {
+        switch (P->block_rows) {
+        case 2: return launch_csr_vector<V, I, 2>(A, b, ldb, epi, st);
+        case 4: return launch_csr_vector<V, I, 4>(A, b, ldb, epi, st);
+        case 8: return launch_csr_vector<V, I, 8>(A, b, ldb, epi, st);
+        case 16: return launch_csr_vector<V, I, 16>(A, b, ldb, epi, st);
+        default: return launch_csr_vector<V, I, 32>(A, b, ldb, epi, st);
+        }
+    }
+    if (kernel == SB_CSR_MERGE) {
+        cudaError_t e = launch_csr_merge<V, I>(A, b, ldb, x_out, ldx, st);
+        if (e != cudaSuccess || is_plain_store<Epi>::value) return e;
+        return launch_epilogue_pass<V, I>(A.rows, x_out, ldx, epi, st);
+    }
+    auto kern = csr_strict_kernel<V, I, Epi>;
+    int grid = persistent_grid(kern, 256, 0);
+    const int64_t need = ceil_div(A.rows, 256);
+    if (grid > need) grid = (int)need;
+    kern<<<grid, 256, 0, st>>>(A.rows, (const I *)A.row_ptrs, (const I *)A.col_idxs,
+                               (const V *)A.values, b, ldb, epi);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- COO
+template <class V, class I>
+cudaError_t coo_raw(const sb_coo &A, const V *b, int64_t ldb, V *x, int64_t ldx, bool accumulate,
+                    cudaStream_t st) {
+    if (A.rows == 0) return cudaSuccess;
+    if (A.nnz == 0) return accumulate ? cudaSuccess : launch_fill<V>(A.rows, 1, x, ldx, (V)0, st);
+    const sb_coo_plan &P = *A.plan;
+    auto kern = coo_kernel<V, I, kCooNT, kCooIPT>;
+    int grid = persistent_grid(kern, kCooNT, 0);
+    if (grid > P.num_tiles) grid = (int)P.num_tiles;
+    kern<<<grid, kCooNT, 0, st>>>(A.rows, A.nnz, (const I *)A.row_idxs, (const I *)A.col_idxs,
+                                  (const V *)A.values, b, ldb, x, ldx, P.num_tiles,
+                                  (int64_t *)P.carry_rows, (double *)P.carry_vals, accumulate);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return launch_fixup<V>(P.num_tiles, (const int64_t *)P.carry_rows, (const double *)P.carry_vals,
+                           x, ldx, st);
+}
+
+template <class V, class I, class Epi>
+cudaError_t coo_apply(const sb_coo &A, const V *b, int64_t ldb, V *x_out, int64_t ldx,
+                      const Epi &epi, cudaStream_t st) {
+    cudaError_t e = coo_raw<V, I>(A, b, ldb, x_out, ldx, false, st);
+    if (e != cudaSuccess || is_plain_store<Epi>::value) return e;
+    return launch_epilogue_pass<V, I>(A.rows, x_out, ldx, epi, st);
+}
+
+// ---------------------------------------------------------------- ELL / SELL-P / Hybrid
+template <class V, class I>
+constexpr int rows_per_thread() {
+    return 16 / sizeof(V);  // one 16-byte value vector per thread per column
+}
+
+template <class V, class I, class Epi>
+cudaError_t ell_apply(const sb_ell &A, const V *b, int64_t ldb, const Epi &epi, cudaStream_t st) {
+    if (A.rows == 0) return cudaSuccess;
+    constexpr int RPT = rows_per_thread<V, I>();
+    const bool vec_ok = (A.stride % RPT == 0) && ((uintptr_t)A.values % 16 == 0) &&
+                        ((uintptr_t)A.col_idxs % (RPT * sizeof(I) >= 16 ? 16 : RPT * sizeof(I)) == 0);
+    if (vec_ok) {
+        auto kern = ell_kernel<V, I, RPT, Epi>;
+        int grid = persistent_grid(kern, 256, 0);
+        const int64_t need = ceil_div(ceil_div(A.rows, RPT), 256);
+        if (grid > need) grid = (int)need;
+        kern<<<grid, 256, 0, st>>>(A.rows, A.width, A.stride, (const I *)A.col_idxs,
+                                   (const V *)A.values, b, ldb, epi);
+    } else {
+        auto kern = ell_kernel<V, I, 1, Epi>;
+        int grid = persistent_grid(kern, 256, 0);
+        const int64_t need = ceil_div(A.rows, 256);
+        if (grid > need) grid = (int)need;
+        kern<<<grid, 256, 0, st>>>(A.rows, A.width, A.stride, (const I *)A.col_idxs,
+                                   (const V *)A.values, b, ldb, epi);
+    }
+    return cudaGetLastError();
+}
+
+template <class V, class I, class Epi>
+cudaError_t sellp_apply(const sb_sellp &A, const V *b, int64_t ldb, const Epi &epi, cudaStream_t st) {
+    if (A.rows == 0) return cudaSuccess;
+    constexpr int RPT = rows_per_thread<V, I>();
+    const bool vec_ok = (A.slice_size % RPT == 0) && ((uintptr_t)A.values % 16 == 0) &&
+                        ((uintptr_t)A.col_idxs % (RPT * sizeof(I) >= 16 ? 16 : RPT * sizeof(I)) == 0);
+    const int64_t slots = A.num_slices * A.slice_size;
+    if (vec_ok) {
+        auto kern = sellp_kernel<V, I, RPT, Epi>;
+        int grid = persistent_grid(kern, 256, 0);
+        const int64_t need = ceil_div(slots / RPT, 256);
+        if (grid > need) grid = (int)(need > 0 ? need : 1);
+        kern<<<grid, 256, 0, st>>>(A.rows, A.slice_size, (const I *)A.slice_lengths,
+                                   (const I *)A.slice_sets, (const I *)A.col_idxs,
+                                   (const V *)A.values, b, ldb, epi);
+    } else {
+        auto kern = sellp_kernel<V, I, 1, Epi>;
+        int grid = persistent_grid(kern, 256, 0);
+        const int64_t need = ceil_div(slots, 256);
+        if (grid > need) grid = (int)(need > 0 ? need : 1);
+        kern<<<grid, 256, 0, st>>>(A.rows, A.slice_size, (const I *)A.slice_lengths,
+                                   (const I *)A.slice_sets, (const I *)A.col_idxs,
+                                   (const V *)A.values, b, ldb, epi);
+    }
+    return cudaGetLastError();
+}
+
+template <class V, class I, class Epi>
+cudaError_t hybrid_apply(const sb_hybrid &A, const V *b, int64_t ldb, V *x_out, int64_t ldx,
+                         const Epi &epi, cudaStream_t st) {
+    cudaError_t e = ell_apply<V, I>(A.ell, b, ldb, EpiStore<V>{x_out, ldx}, st);
+    if (e != cudaSuccess) return e;
+    if (A.coo.nnz > 0) {
+        e = coo_raw<V, I>(A.coo, b, ldb, x_out, ldx, true, st);
+        if (e != cudaSuccess) return e;
+    }
+    if (is_plain_store<Epi>::value) return cudaSuccess;
+    return launch_epilogue_pass<V, I>(A.ell.rows, x_out, ldx, epi, st);
+}
+
+// ---------------------------------------------------------------- any format
+template <class V, class I, class Epi>
+cudaError_t matrix_apply(const sb_matrix &M, const V *b, int64_t ldb, V *x_out, int64_t ldx,
+                         const Epi &epi, cudaStream_t st) {
+    switch (M.format) {
+    case SB_FMT_CSR: return csr_apply<V, I>(*(const sb_csr *)M.mat, b, ldb, x_out, ldx, epi, st);
+    case SB_FMT_COO: return coo_apply<V, I>(*(const sb_coo *)M.mat, b, ldb, x_out, ldx, epi, st);
+    case SB_FMT_ELL: return ell_apply<V, I>(*(const sb_ell *)M.mat, b, ldb, epi, st);
+    case SB_FMT_SELLP: return sellp_apply<V, I>(*(const sb_sellp *)M.mat, b, ldb, epi, st);
+    case SB_FMT_HYBRID:
+        return hybrid_apply<V, I>(*(const sb_hybrid *)M.mat, b, ldb, x_out, ldx, epi, st);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+inline int64_t matrix_rows(const sb_matrix &M) {
+    switch (M.format) {
+    case SB_FMT_CSR: return ((const sb_csr *)M.mat)->rows;
+    case SB_FMT_COO: return ((const sb_coo *)M.mat)->rows;
+    case SB_FMT_ELL: return ((const sb_ell *)M.mat)->rows;
+    case SB_FMT_SELLP: return ((const sb_sellp *)M.mat)->rows;
+    case SB_FMT_HYBRID: return ((const sb_hybrid *)M.mat)->ell.rows;
+    default: return -1;
+    }
+}
+inline int64_t matrix_cols(const sb_matrix &M) {
+    switch (M.format) {
+    case SB_FMT_CSR: return ((const sb_csr *)M.mat)->cols;
+    case SB_FMT_COO: return ((const sb_coo *)M.mat)->cols;
+    case SB_FMT_ELL: return ((const sb_ell *)M.mat)->cols;
+    case SB_FMT_SELLP: return ((const sb_sellp *)M.mat)->cols;
+    case SB_FMT_HYBRID: return ((const sb_hybrid *)M.mat)->ell.cols;
+    default: return -1;
+    }
+}
+
+}  // namespace sb

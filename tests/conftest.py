@@ -33,3 +33,10 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+@pytest.fixture(scope="session")
+def dev():
+    from paper_2510_08230_b200 import sparseops as sp
+
+    return sp.create_device("cuda", 0)

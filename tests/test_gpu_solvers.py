@@ -1,0 +1,181 @@
+"""GPU parity: the device Krylov solvers against the reference.
+
+Bar (north_star): iteration counts within +-2% of the reference, same stop reason,
+recurrence residual below the tolerance; the true residual is reported beside it.
+The only numerical difference from the reference is the order of the fp64 dot sums,
+so histories agree to ~1e-10 relative in the early iterations.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import fixtures, sbref
+from paper_2510_08230_b200 import gen
+from paper_2510_08230_b200 import sparseops as sp
+from tests import golden_io
+from tests.gpu_util import csr, host, out, vec
+
+pytestmark = pytest.mark.gpu
+
+SOLVERS = {"cg": sp.Cg, "cgs": sp.Cgs, "gmres": sp.Gmres, "bicgstab": sp.Bicgstab}
+
+
+def within(n, ref, pct=0.02):
+    return abs(n - ref) <= max(1, int(np.ceil(pct * ref)))
+
+
+def true_residual(rp, ci, v, b, x):
+    r = b.astype(np.float64) - sbref.csr_spmv(rp, ci, v.astype(np.float64), x.astype(np.float64))
+    return np.linalg.norm(r) / max(np.linalg.norm(b), 1e-300)
+
+
+def solve(dev, kind, a, bvec, criteria, precond=True, x0=None, **kw):
+    m = sp.jacobi_create(a) if precond else None
+    b = vec(dev, bvec)
+    x = vec(dev, np.zeros(a.rows, bvec.dtype) if x0 is None else x0)
+    log = SOLVERS[kind](a, criteria=criteria, preconditioner=m, **kw).solve(b, x)
+    return log, host(x), b
+
+
+def test_reference_solver_goldens(dev):
+    """Every reference run recorded in tests/golden/solvers.json."""
+    meta = golden_io.solver_meta()
+    g = golden_io.load("solvers.npz")
+    for name, m in meta.items():
+        if name.startswith("_"):
+            continue
+        dt = np.dtype(m["dtype"])
+        a = gen.stencil_csr(dev, m["p"], dim=3, c=m["c"], precision=sp.Precision.from_dtype(dt))
+        crit = [sp.Iteration(m["max_iters"])] + (
+            [sp.ResidualNorm(m["reduction_factor"])] if m["reduction_factor"] else [])
+        kw = {"krylov_dim": m["krylov_dim"]} if m["solver"] == "gmres" else {}
+        log, x, _ = solve(dev, m["solver"], a, np.ones(a.rows, dt), crit, **kw)
+        assert log.stop_reason == m["stop_reason"], name
+        assert log.converged == m["converged"], name
+        if m["stop_reason"] == "max_iters":
+            assert log.iterations == m["iterations"], name
+        else:
+            assert within(log.iterations, m["iterations"]), (name, log.iterations, m["iterations"])
+        hist = np.asarray(log.residual_history)
+        ref = g[f"{name}_history"]
+        k = min(10, len(ref), len(hist))
+        np.testing.assert_allclose(hist[:k], ref[:k], rtol=1e-6 if dt == np.float32 else 1e-9,
+                                   err_msg=name)
+        xref = g[f"{name}_x"]
+        rel = np.abs(x.astype(np.float64) - xref).max() / np.abs(xref).max()
+        assert rel <= (1e-3 if dt == np.float32 else 1e-6), (name, rel)
+
+
+@pytest.mark.parametrize("p,iters", [(64, 159), (128, 319)])
+def test_cg_poisson_config2_iteration_parity(dev, p, iters):
+    """Config #2 (and 64^3): Jacobi-CG, b = 1, x0 = 0, rtol 1e-8 -> the reference's
+    iteration count (SURVEY.md §8c golden, 319 at 128^3) within +-2%."""
+    a = gen.poisson3d(dev, p)
+    log, x, _ = solve(dev, "cg", a, np.ones(a.rows), [sp.Iteration(100000), sp.ResidualNorm(1e-8)])
+    assert log.converged and within(log.iterations, iters), log.iterations
+    assert log.residual_history[-1] <= 1e-8 * np.sqrt(a.rows)
+    rp, ci, v = (t.cpu().numpy() for t in (a.row_ptrs, a.col_idxs, a.values))
+    assert true_residual(rp, ci, v, np.ones(a.rows), x) <= 2e-8
+
+
+def test_gmres_convdiff_64(dev):
+    a = gen.convdiff3d(dev, 64)
+    log, x, _ = solve(dev, "gmres", a, np.ones(a.rows), [sp.Iteration(5000), sp.ResidualNorm(1e-8)],
+                      krylov_dim=30)
+    assert log.converged and within(log.iterations, 330), log.iterations
+
+
+@pytest.mark.parametrize("p", [16, 32])
+def test_bicgstab_against_oracle(dev, p):
+    """BiCGSTAB has no reference implementation: parity with the oracle restatement."""
+    for c in (0.0, 0.5):
+        a = gen.stencil_csr(dev, p, dim=3, c=c)
+        rp, ci, v = (t.cpu().numpy() for t in (a.row_ptrs, a.col_idxs, a.values))
+        inv, _ = sbref.jacobi_create(rp, ci, v)
+        ref, xref = sbref.solve("bicgstab", rp, ci, v, np.ones(a.rows), inv_diag=inv,
+                                max_iters=5000, reduction_factor=1e-8)
+        log, x, _ = solve(dev, "bicgstab", a, np.ones(a.rows),
+                          [sp.Iteration(5000), sp.ResidualNorm(1e-8)])
+        assert log.converged and ref.converged
+        assert within(log.iterations, ref.iterations), (log.iterations, ref.iterations)
+        np.testing.assert_allclose(log.residual_history[:5], ref.residual_history[:5], rtol=1e-9)
+        assert true_residual(rp, ci, v, np.ones(a.rows), x) <= 1e-7
+
+
+@pytest.mark.parametrize("kind", ["cg", "cgs", "gmres", "bicgstab"])
+def test_every_format_same_iterations(dev, kind):
+    c = 0.0 if kind == "cg" else 0.5
+    a = gen.stencil_csr(dev, 20, dim=3, c=c)
+    crit = [sp.Iteration(3000), sp.ResidualNorm(1e-8)]
+    base, _, _ = solve(dev, kind, a, np.ones(a.rows), crit)
+    mats = [a.with_kernel("strict"), a.with_kernel("vector"), a.with_kernel("merge"),
+            sp.coo_from_csr(a), sp.ell_from_csr(a), sp.sellp_from_csr(a), sp.hybrid_from_csr(a, 5)]
+    for m in mats:
+        log, _, _ = solve(dev, kind, m, np.ones(a.rows), crit)
+        assert log.converged and within(log.iterations, base.iterations), (repr(m), log.iterations)
+    # polled (non-graph) loop gives the identical run
+    from paper_2510_08230_b200 import _lib
+    _lib.fn("sb_set_graph_mode")(0)
+    try:
+        polled, _, _ = solve(dev, kind, a, np.ones(a.rows), crit)
+    finally:
+        _lib.fn("sb_set_graph_mode")(1)
+    assert polled.iterations == base.iterations
+    assert polled.residual_history == base.residual_history
+
+
+def test_semantics(dev):
+    """test_solvers.py:79-145 behaviours on the device."""
+    one = sp.csr_from_dense(dev, np.eye(4))
+    log, x, _ = solve(dev, "cg", one, np.ones(4), [sp.Iteration(1000), sp.ResidualNorm(1e-6)],
+                      precond=False)
+    assert log.iterations == 1 and log.converged and log.residual_history[-1] == 0.0
+    np.testing.assert_allclose(x, 1.0)
+    zero = sp.csr_from_dense(dev, np.zeros((2, 2)), keep_zeros=False)
+    with pytest.raises(sp.errors.BreakdownError) as exc:
+        solve(dev, "cg", zero, np.array([1.0, 2.0]), [sp.Iteration(10)], precond=False)
+    assert exc.value.iteration == 1
+    with pytest.raises(sp.errors.BreakdownError) as exc:
+        solve(dev, "cgs", zero, np.array([1.0, 2.0]), [sp.Iteration(10)], precond=False)
+    assert exc.value.iteration == 1
+    d = sp.csr_from_dense(dev, np.diag([2.0, 4.0]))
+    for kind in SOLVERS:
+        log, _, _ = solve(dev, kind, d, np.array([2.0, 4.0]), [sp.Iteration(10), sp.ResidualNorm(1e-6)],
+                          precond=False, x0=np.array([1.0, 1.0]))
+        assert log.iterations == 0 and log.converged and log.residual_history == [0.0], kind
+    # fixed-iteration mode runs exactly max_iters (test_solvers.py:296-313)
+    a = gen.poisson3d(dev, 8)
+    for kind in SOLVERS:
+        log, _, _ = solve(dev, kind, a, np.ones(a.rows), [sp.Iteration(7)], krylov_dim=3) \
+            if kind == "gmres" else solve(dev, kind, a, np.ones(a.rows), [sp.Iteration(7)])
+        assert log.iterations == 7 and log.stop_reason == "max_iters", kind
+        assert len(log.residual_history) == 7
+    # b untouched, x overwritten
+    bv = np.random.default_rng(2).random(a.rows)
+    b = vec(dev, bv)
+    x = vec(dev, np.full(a.rows, 0.5))
+    sp.Cg(a, criteria=[sp.Iteration(100), sp.ResidualNorm(1e-10)]).solve(b, x)
+    np.testing.assert_array_equal(host(b), bv)
+
+
+def test_fp32_cg(dev):
+    a = gen.poisson3d(dev, 16, precision=sp.Precision.single)
+    log, x, _ = solve(dev, "cg", a, np.ones(a.rows, np.float32),
+                      [sp.Iteration(1000), sp.ResidualNorm(1e-5)])
+    assert log.converged and within(log.iterations, 28)
+
+
+def test_config_solve_listing2(dev):
+    tree = {"type": "solver::Gmres", "krylov_dim": 30,
+            "preconditioner": {"type": "preconditioner::Jacobi"},
+            "criteria": [{"type": "Iteration", "max_iters": 1000},
+                         {"type": "ResidualNorm", "reduction_factor": 1e-8}]}
+    a = gen.convdiff3d(dev, 16)
+    b = sp.dense_create(dev, a.rows, 1, sp.Precision.double, 1.0)
+    x = sp.dense_create(dev, a.rows, 1, sp.Precision.double, 0.0)
+    log, res = sp.config_solve(tree, dev, a, b, x)
+    assert res is x and log.converged and within(log.iterations, 81)
+    tree["type"] = "solver::Bicgstab"
+    del tree["krylov_dim"]
+    log, _ = sp.config_solve(tree, dev, a, b, sp.dense_create(dev, a.rows, 1, sp.Precision.double, 0.0))
+    assert log.converged
