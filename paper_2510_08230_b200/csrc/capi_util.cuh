@@ -54,7 +54,9 @@ inline sb_status cuda_fail(sb_error *err, cudaError_t e, const char *where) {
 
 inline cudaStream_t as_stream(sb_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
-// reduction workspace layout: [0, 256) tickets / scalars, [256, ...) partials
+// reduction workspace layout: [0, 64) tickets, [64, 128) result scalars,
+// [128, 256) scratch (row statistics / first-bad-row flags), [256, ...) partials
+constexpr size_t kReduceScratch = 128;
 constexpr size_t kReduceHeader = 256;
 constexpr size_t kReduceBytes = 256 + 3 * 8 * 4096;
 

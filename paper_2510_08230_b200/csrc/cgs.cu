@@ -60,7 +60,7 @@ struct EpiCgsResidual {
     const V *rs;
     Ctl *ctl;
     double *partials;
-    __device__ __forceinline__ bool skip() const { return ctl->done != 0; }
+    __device__ __forceinline__ bool skip() const { return loop_done(ctl); }
     __device__ __forceinline__ void row(int64_t i, double acc, double (&part)[N]) const {
         const V ti = (V)acc;
         t[i] = ti;

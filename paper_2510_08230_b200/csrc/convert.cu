@@ -363,7 +363,7 @@ sb_status jacobi_create(const sb_csr *a, void *inv, void *ws, cudaStream_t st, s
     if (a->rows != a->cols)
         return fail(err, SB_ERR_DIMENSION_MISMATCH, "expected a square matrix, got %lldx%lld",
                     (long long)a->rows, (long long)a->cols);
-    unsigned long long *bad = (unsigned long long *)ws;
+    unsigned long long *bad = (unsigned long long *)((unsigned char *)ws + kReduceScratch);
     init_bad_kernel<<<1, 32, 0, st>>>(bad);
     if (a->rows > 0)
         jacobi_kernel<V, I><<<elem_grid(a->rows), 256, 0, st>>>(

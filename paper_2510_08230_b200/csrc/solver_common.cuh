@@ -62,6 +62,17 @@ __device__ __forceinline__ void stop_loop(Ctl *c) {
     if (c->cond) cudaGraphSetConditional((cudaGraphConditionalHandle)c->cond, 0);
 }
 
+// Entry test of every loop kernel: a finished solve turns the kernel into a no-op, and
+// (inside the graph) clears the WHILE condition -- this also ends a loop whose setup
+// finished the solve (exact initial guess) before the graph was launched.  ctl->cond
+// is only non-zero while the graph runs, so setup kernels never touch the handle.
+__device__ __forceinline__ bool loop_done(const Ctl *c) {
+    if (!c->done) return false;
+    if (c->cond && blockIdx.x == 0 && threadIdx.x == 0)
+        cudaGraphSetConditional((cudaGraphConditionalHandle)c->cond, 0);
+    return true;
+}
+
 // solvers.check_criteria (solvers.py:121-135): residual wins ties
 __device__ __forceinline__ int check_criteria(const Ctl *c, int64_t it, double res, double bnorm) {
     if (c->has_rf) {
@@ -98,7 +109,7 @@ inline int solver_grid() { return device_info().sms * 4; }
 
 template <int N, class Op>
 __global__ void __launch_bounds__(256) ew_kernel(int64_t n, Ctl *ctl, double *partials, Op op) {
-    if (ctl->done || op.skip(ctl)) return;
+    if (loop_done(ctl) || op.skip(ctl)) return;
     op.prepare(ctl);
     double part[N > 0 ? N : 1] = {};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -121,7 +132,7 @@ cudaError_t launch_ew(int64_t n, Ctl *ctl, double *partials, const Op &op, cudaS
 // single-thread scalar step (host-free control logic between passes)
 template <class Op>
 __global__ void scalar_kernel(Ctl *ctl, Op op) {
-    if (ctl->done || op.skip(ctl)) return;
+    if (loop_done(ctl) || op.skip(ctl)) return;
     op.run(ctl);
 }
 
@@ -135,7 +146,7 @@ struct EpiSolver {
     Ctl *ctl;
     double *partials;
     Fin fin;
-    __device__ __forceinline__ bool skip() const { return ctl->done || fin.skip(ctl); }
+    __device__ __forceinline__ bool skip() const { return loop_done(ctl) || fin.skip(ctl); }
     __device__ __forceinline__ void row(int64_t i, double acc, double (&part)[N]) const {
         const V yi = (V)acc;
         y[i] = yi;
@@ -155,7 +166,7 @@ struct EpiSolverStore {
     V *y;
     Ctl *ctl;
     Skip sk;
-    __device__ __forceinline__ bool skip() const { return ctl->done || sk.skip(ctl); }
+    __device__ __forceinline__ bool skip() const { return loop_done(ctl) || sk.skip(ctl); }
     __device__ __forceinline__ void row(int64_t i, double acc, double (&)[N]) const { y[i] = (V)acc; }
     __device__ __forceinline__ void finish(double (&)[N]) const {}
 };

@@ -98,10 +98,14 @@ sb_status run_loop(const LoopSpec &spec, Ctl *dctl, Ctl &hctl, cudaStream_t st, 
         }
         if (use_graph) entry = it->second;
     }
-    hctl.cond = use_graph ? (unsigned long long)entry.handle : 0ull;
+    hctl.cond = 0ull;  // setup kernels run outside the graph: no handle yet
     SB_CUDA(cudaMemcpyAsync(dctl, &hctl, sizeof(Ctl), cudaMemcpyHostToDevice, st));
     SB_CUDA(spec.setup(st));
     if (use_graph) {
+        static thread_local unsigned long long handle_value;
+        handle_value = (unsigned long long)entry.handle;
+        SB_CUDA(cudaMemcpyAsync(&dctl->cond, &handle_value, sizeof(handle_value),
+                                cudaMemcpyHostToDevice, st));
         SB_CUDA(cudaGraphLaunch(entry.exec, st));
     } else {
         static thread_local int *pinned = nullptr;

@@ -66,7 +66,7 @@ sb_status row_stats(int64_t rows, const void *row_ptrs, void *ws, sb_row_stats *
                     cudaStream_t st, sb_error *err) {
     if (!out || !ws || (rows > 0 && !row_ptrs))
         return fail(err, SB_ERR_INVALID_ARGUMENT, "row_stats: null argument");
-    unsigned long long *acc = (unsigned long long *)ws;
+    unsigned long long *acc = (unsigned long long *)((unsigned char *)ws + kReduceScratch);
     stats_init_kernel<<<1, 32, 0, st>>>(acc);
     if (rows > 0)
         row_stats_kernel<I><<<elem_grid(rows), 256, 0, st>>>(rows, (const I *)row_ptrs, acc);

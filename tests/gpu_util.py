@@ -32,8 +32,8 @@ def scale(row_ptrs, values, b):
     """max_i sum_j |a_ij| * max|b| (test_acceptance.py:80-87 scale)."""
     rp = np.asarray(row_ptrs, np.int64)
     absv = np.abs(np.asarray(values, np.float64))
-    rs = np.add.reduceat(absv, rp[:-1]) if absv.size else np.zeros(len(rp) - 1)
-    rs[np.diff(rp) == 0] = 0.0
+    rows = np.repeat(np.arange(len(rp) - 1), np.diff(rp))
+    rs = np.bincount(rows, weights=absv, minlength=len(rp) - 1)
     mx = rs.max(initial=0.0)
     return max(mx * max(np.abs(np.asarray(b, np.float64)).max(initial=0.0), 1e-30), 1e-30)
 
