@@ -198,6 +198,10 @@ def load(path: str = LIB_PATH):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
+        if os.environ.get("SPARSEB200_GRAPH", "1") == "0":
+            # host-polled solver loops (profilers cannot see kernels inside graphs
+            # that contain conditional nodes); same kernels, same order
+            lib.sb_set_graph_mode(0)
         _lib = lib
         return lib
 

@@ -15,6 +15,7 @@ struct SkipEarly {
 // phat = M p
 template <class V>
 struct BiDirection : SkipNone {
+    using value_type = V;
     const V *r, *v, *inv;
     V *p, *ph;
     double beta, omega;
@@ -24,27 +25,46 @@ struct BiDirection : SkipNone {
         omega = c->omega;
         first = c->iter == 0;
     }
+    template <int W>
     __device__ __forceinline__ void elem(int64_t i, double (&)[1]) const {
-        V pi;
-        if (first) pi = r[i];
-        else pi = axpy_e(1.0, r[i], scal_e(beta, axpy_e(-omega, v[i], p[i])));
-        p[i] = pi;
-        ph[i] = precond_e(inv, i, pi);
+        const auto R = ldp<W>(r, i), D = ldp_or_one<W>(inv, i);
+        Pk<V, W> P, PH;
+        if (first) {
+            P = R;
+        } else {
+            const auto Vv = ldp<W>(v, i);
+            P = ldp<W>(p, i);
+#pragma unroll
+            for (int w = 0; w < W; ++w)
+                P.v[w] = axpy_e(1.0, R.v[w], scal_e(beta, axpy_e(-omega, Vv.v[w], P.v[w])));
+        }
+#pragma unroll
+        for (int w = 0; w < W; ++w) PH.v[w] = inv ? vmul(P.v[w], D.v[w]) : P.v[w];
+        stp<W>(p, i, P);
+        stp<W>(ph, i, PH);
     }
 };
 
 // s = r - alpha v; shat = M s; ||s|| may stop early (x += alpha phat follows)
 template <class V>
 struct BiS : SkipNone {
+    using value_type = V;
     const V *r, *v, *inv;
     V *s, *sh;
     double alpha;
     __device__ __forceinline__ void prepare(const Ctl *c) { alpha = c->alpha; }
+    template <int W>
     __device__ __forceinline__ void elem(int64_t i, double (&part)[1]) const {
-        const V si = axpy_e(-alpha, v[i], r[i]);
-        s[i] = si;
-        sh[i] = precond_e(inv, i, si);
-        part[0] = addd(part[0], mulp(si, si));
+        const auto R = ldp<W>(r, i), Vv = ldp<W>(v, i), D = ldp_or_one<W>(inv, i);
+        Pk<V, W> S, SH;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            S.v[w] = axpy_e(-alpha, Vv.v[w], R.v[w]);
+            SH.v[w] = inv ? vmul(S.v[w], D.v[w]) : S.v[w];
+            part[0] = addd(part[0], mulp(S.v[w], S.v[w]));
+        }
+        stp<W>(s, i, S);
+        stp<W>(sh, i, SH);
     }
     __device__ __forceinline__ void last(Ctl *c, const double (&tot)[1]) const {
         const double snorm = sqrt(tot[0]);
@@ -59,14 +79,19 @@ struct BiS : SkipNone {
 // early stop: x += alpha phat, then finish
 template <class V>
 struct BiEarlyX {
+    using value_type = V;
     const V *ph;
     V *x;
     double alpha;
     __device__ __forceinline__ bool skip(const Ctl *c) const { return c->early == 0; }
     __device__ __forceinline__ void prepare(const Ctl *c) { alpha = c->alpha; }
-    __device__ __forceinline__ void elem(int64_t i, double (&part)[1]) const {
-        x[i] = axpy_e(alpha, ph[i], x[i]);
-        (void)part;
+    template <int W>
+    __device__ __forceinline__ void elem(int64_t i, double (&)[1]) const {
+        const auto PH = ldp<W>(ph, i);
+        auto X = ldp<W>(x, i);
+#pragma unroll
+        for (int w = 0; w < W; ++w) X.v[w] = axpy_e(alpha, PH.v[w], X.v[w]);
+        stp<W>(x, i, X);
     }
     __device__ __forceinline__ void last(Ctl *c, const double (&)[1]) const {
         finish_with(c, c->iter, STOP_RESIDUAL);
@@ -89,6 +114,7 @@ struct BiOmegaFin {
 // x += alpha phat + omega shat; r = s - omega t; dots r.r, rhat.r (next rho)
 template <class V>
 struct BiUpdate : SkipEarly {
+    using value_type = V;
     const V *ph, *sh, *s, *t, *rh;
     V *x, *r;
     double alpha, omega;
@@ -96,12 +122,21 @@ struct BiUpdate : SkipEarly {
         alpha = c->alpha;
         omega = c->omega;
     }
+    template <int W>
     __device__ __forceinline__ void elem(int64_t i, double (&part)[2]) const {
-        x[i] = axpy_e(omega, sh[i], axpy_e(alpha, ph[i], x[i]));
-        const V ri = axpy_e(-omega, t[i], s[i]);
-        r[i] = ri;
-        part[0] = addd(part[0], mulp(ri, ri));
-        part[1] = addd(part[1], mulp(rh[i], ri));
+        const auto PH = ldp<W>(ph, i), SH = ldp<W>(sh, i), S = ldp<W>(s, i), T = ldp<W>(t, i),
+                   RH = ldp<W>(rh, i);
+        auto X = ldp<W>(x, i);
+        Pk<V, W> R;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            X.v[w] = axpy_e(omega, SH.v[w], axpy_e(alpha, PH.v[w], X.v[w]));
+            R.v[w] = axpy_e(-omega, T.v[w], S.v[w]);
+            part[0] = addd(part[0], mulp(R.v[w], R.v[w]));
+            part[1] = addd(part[1], mulp(RH.v[w], R.v[w]));
+        }
+        stp<W>(x, i, X);
+        stp<W>(r, i, R);
     }
     __device__ __forceinline__ void last(Ctl *c, const double (&tot)[2]) const {
         const int64_t it = c->iter;

@@ -9,18 +9,24 @@ namespace sb {
 // setup: r = b - A x (t = A x first), z = M r, p = z; dots b.b, r.r, r.z
 template <class V>
 struct CgInit : SkipNone {
+    using value_type = V;
     const V *b, *t, *inv;
     V *r, *z, *p;
+    template <int W>
     __device__ __forceinline__ void elem(int64_t i, double (&part)[3]) const {
-        const V bi = b[i];
-        const V ri = axpy_e(-1.0, t[i], bi);
-        const V zi = precond_e(inv, i, ri);
-        r[i] = ri;
-        z[i] = zi;
-        p[i] = zi;
-        part[0] = addd(part[0], mulp(bi, bi));
-        part[1] = addd(part[1], mulp(ri, ri));
-        part[2] = addd(part[2], mulp(ri, zi));
+        const auto B = ldp<W>(b, i), T = ldp<W>(t, i), D = ldp_or_one<W>(inv, i);
+        Pk<V, W> R, Z;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            R.v[w] = axpy_e(-1.0, T.v[w], B.v[w]);
+            Z.v[w] = inv ? vmul(R.v[w], D.v[w]) : R.v[w];
+            part[0] = addd(part[0], mulp(B.v[w], B.v[w]));
+            part[1] = addd(part[1], mulp(R.v[w], R.v[w]));
+            part[2] = addd(part[2], mulp(R.v[w], Z.v[w]));
+        }
+        stp<W>(r, i, R);
+        stp<W>(z, i, Z);
+        stp<W>(p, i, Z);
     }
     __device__ __forceinline__ void last(Ctl *c, const double (&tot)[3]) const {
         c->bnorm = sqrt(tot[0]);
@@ -57,18 +63,27 @@ struct CgPqFin {
 // x += alpha p; r -= alpha q; z = M r; dots r.r, r.z -> criteria, beta (solvers.py:207-222)
 template <class V>
 struct CgUpdate : SkipNone {
+    using value_type = V;
     const V *p, *q, *inv;
     V *x, *r, *z;
     double alpha;
     __device__ __forceinline__ void prepare(const Ctl *c) { alpha = c->alpha; }
+    template <int W>
     __device__ __forceinline__ void elem(int64_t i, double (&part)[2]) const {
-        x[i] = axpy_e(alpha, p[i], x[i]);
-        const V ri = axpy_e(-alpha, q[i], r[i]);
-        const V zi = precond_e(inv, i, ri);
-        r[i] = ri;
-        z[i] = zi;
-        part[0] = addd(part[0], mulp(ri, ri));
-        part[1] = addd(part[1], mulp(ri, zi));
+        const auto P = ldp<W>(p, i), Q = ldp<W>(q, i), D = ldp_or_one<W>(inv, i);
+        auto X = ldp<W>(x, i), R = ldp<W>(r, i);
+        Pk<V, W> Z;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            X.v[w] = axpy_e(alpha, P.v[w], X.v[w]);
+            R.v[w] = axpy_e(-alpha, Q.v[w], R.v[w]);
+            Z.v[w] = inv ? vmul(R.v[w], D.v[w]) : R.v[w];
+            part[0] = addd(part[0], mulp(R.v[w], R.v[w]));
+            part[1] = addd(part[1], mulp(R.v[w], Z.v[w]));
+        }
+        stp<W>(x, i, X);
+        stp<W>(r, i, R);
+        stp<W>(z, i, Z);
     }
     __device__ __forceinline__ void last(Ctl *c, const double (&tot)[2]) const {
         const int64_t it = c->iter;
@@ -94,12 +109,18 @@ struct CgUpdate : SkipNone {
 // p = z + beta p  (scal(beta, p); axpy(1, z, p))
 template <class V>
 struct CgDirection : SkipNone {
+    using value_type = V;
     const V *z;
     V *p;
     double beta;
     __device__ __forceinline__ void prepare(const Ctl *c) { beta = c->beta; }
+    template <int W>
     __device__ __forceinline__ void elem(int64_t i, double (&)[1]) const {
-        p[i] = axpy_e(1.0, z[i], scal_e(beta, p[i]));
+        const auto Z = ldp<W>(z, i);
+        auto P = ldp<W>(p, i);
+#pragma unroll
+        for (int w = 0; w < W; ++w) P.v[w] = axpy_e(1.0, Z.v[w], scal_e(beta, P.v[w]));
+        stp<W>(p, i, P);
     }
 };
 

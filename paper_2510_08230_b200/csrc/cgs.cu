@@ -10,6 +10,7 @@ namespace sb {
 // copy/scal/axpy rounding; phat = M p
 template <class V>
 struct CgsDirection : SkipNone {
+    using value_type = V;
     const V *r, *q, *inv;
     V *u, *p, *ph;
     double beta;
@@ -18,37 +19,54 @@ struct CgsDirection : SkipNone {
         beta = c->beta;
         first = c->iter == 0;
     }
+    template <int W>
     __device__ __forceinline__ void elem(int64_t i, double (&)[1]) const {
-        V ui, pi;
+        const auto R = ldp<W>(r, i), D = ldp_or_one<W>(inv, i);
+        Pk<V, W> U, P, PH;
         if (first) {
-            ui = r[i];
-            pi = ui;
+            U = R;
+            P = R;
         } else {
-            const V qi = q[i];
-            ui = axpy_e(1.0, r[i], scal_e(beta, qi));
-            pi = axpy_e(1.0, ui, axpy_e(beta, qi, scal_e(__dmul_rn(beta, beta), p[i])));
+            const auto Q = ldp<W>(q, i);
+            P = ldp<W>(p, i);
+            const double b2 = __dmul_rn(beta, beta);
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                U.v[w] = axpy_e(1.0, R.v[w], scal_e(beta, Q.v[w]));
+                P.v[w] = axpy_e(1.0, U.v[w], axpy_e(beta, Q.v[w], scal_e(b2, P.v[w])));
+            }
         }
-        u[i] = ui;
-        p[i] = pi;
-        ph[i] = precond_e(inv, i, pi);
+#pragma unroll
+        for (int w = 0; w < W; ++w) PH.v[w] = inv ? vmul(P.v[w], D.v[w]) : P.v[w];
+        stp<W>(u, i, U);
+        stp<W>(p, i, P);
+        stp<W>(ph, i, PH);
     }
 };
 
 // q = u - alpha v; uhat = M (u + q); x += alpha uhat
 template <class V>
 struct CgsQ : SkipNone {
+    using value_type = V;
     const V *u, *v, *inv;
     V *q, *uh, *x;
     double alpha;
     __device__ __forceinline__ void prepare(const Ctl *c) { alpha = c->alpha; }
+    template <int W>
     __device__ __forceinline__ void elem(int64_t i, double (&)[1]) const {
-        const V ui = u[i];
-        const V qi = axpy_e(-alpha, v[i], ui);
-        const V uq = axpy_e(1.0, qi, ui);
-        const V uhi = precond_e(inv, i, uq);
-        q[i] = qi;
-        uh[i] = uhi;
-        x[i] = axpy_e(alpha, uhi, x[i]);
+        const auto U = ldp<W>(u, i), Vv = ldp<W>(v, i), D = ldp_or_one<W>(inv, i);
+        auto X = ldp<W>(x, i);
+        Pk<V, W> Q, UH;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            Q.v[w] = axpy_e(-alpha, Vv.v[w], U.v[w]);
+            const V uq = axpy_e(1.0, Q.v[w], U.v[w]);
+            UH.v[w] = inv ? vmul(uq, D.v[w]) : uq;
+            X.v[w] = axpy_e(alpha, UH.v[w], X.v[w]);
+        }
+        stp<W>(q, i, Q);
+        stp<W>(uh, i, UH);
+        stp<W>(x, i, X);
     }
 };
 
@@ -98,15 +116,22 @@ struct EpiCgsResidual {
 // the same update as a separate pass for row-splitting formats (t already written)
 template <class V>
 struct CgsResidualPass : SkipNone {
+    using value_type = V;
     const V *t, *rs;
     V *r;
     double alpha;
     __device__ __forceinline__ void prepare(const Ctl *c) { alpha = c->alpha; }
+    template <int W>
     __device__ __forceinline__ void elem(int64_t i, double (&part)[2]) const {
-        const V ri = axpy_e(-alpha, t[i], r[i]);
-        r[i] = ri;
-        part[0] = addd(part[0], mulp(ri, ri));
-        part[1] = addd(part[1], mulp(rs[i], ri));
+        const auto T = ldp<W>(t, i), RS = ldp<W>(rs, i);
+        auto R = ldp<W>(r, i);
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            R.v[w] = axpy_e(-alpha, T.v[w], R.v[w]);
+            part[0] = addd(part[0], mulp(R.v[w], R.v[w]));
+            part[1] = addd(part[1], mulp(RS.v[w], R.v[w]));
+        }
+        stp<W>(r, i, R);
     }
     __device__ __forceinline__ void last(Ctl *c, const double (&tot)[2]) const {
         EpiCgsResidual<V>::last(c, tot);

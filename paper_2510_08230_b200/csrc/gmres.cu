@@ -19,12 +19,19 @@ struct SkipUnlessCycleEnd {
 // restart: r = b - A x, beta = ||r||; reset the cycle's small dense state
 template <class V>
 struct GmRestart : SkipNone {
+    using value_type = V;
     const V *b, *t;
     V *r;
+    template <int W>
     __device__ __forceinline__ void elem(int64_t i, double (&part)[1]) const {
-        const V ri = axpy_e(-1.0, t[i], b[i]);
-        r[i] = ri;
-        part[0] = addd(part[0], mulp(ri, ri));
+        const auto B = ldp<W>(b, i), T = ldp<W>(t, i);
+        Pk<V, W> R;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            R.v[w] = axpy_e(-1.0, T.v[w], B.v[w]);
+            part[0] = addd(part[0], mulp(R.v[w], R.v[w]));
+        }
+        stp<W>(r, i, R);
     }
     __device__ __forceinline__ void last(Ctl *c, const double (&tot)[1]) const {
         const double beta = sqrt(tot[0]);
@@ -49,19 +56,34 @@ struct GmRestart : SkipNone {
 // v0 = (1 / beta) r  (copy + scal(1.0 / beta))
 template <class V>
 struct GmFirstBasis : SkipNone {
+    using value_type = V;
     const V *r;
     V *v0;
     double inv_beta;
     __device__ __forceinline__ void prepare(const Ctl *c) { inv_beta = 1.0 / c->beta_restart; }
-    __device__ __forceinline__ void elem(int64_t i, double (&)[1]) const { v0[i] = scal_e(inv_beta, r[i]); }
+    template <int W>
+    __device__ __forceinline__ void elem(int64_t i, double (&)[1]) const {
+        auto R = ldp<W>(r, i);
+#pragma unroll
+        for (int w = 0; w < W; ++w) R.v[w] = scal_e(inv_beta, R.v[w]);
+        stp<W>(v0, i, R);
+    }
 };
 
 // z = M v_j
 template <class V>
 struct GmPrecond : SkipCycleEnd {
+    using value_type = V;
     const V *vj, *inv;
     V *z;
-    __device__ __forceinline__ void elem(int64_t i, double (&)[1]) const { z[i] = vmul(vj[i], inv[i]); }
+    template <int W>
+    __device__ __forceinline__ void elem(int64_t i, double (&)[1]) const {
+        auto Z = ldp<W>(vj, i);
+        const auto D = ldp<W>(inv, i);
+#pragma unroll
+        for (int w = 0; w < W; ++w) Z.v[w] = vmul(Z.v[w], D.v[w]);
+        stp<W>(z, i, Z);
+    }
 };
 
 // w = A z with h_0j = v_0.w fused
@@ -73,15 +95,22 @@ struct GmH0Fin {
 // one MGS step: w -= h_i v_i, then h_{i+1} = v_{i+1}.w (single pass)
 template <class V>
 struct GmMgsStep : SkipCycleEnd {
+    using value_type = V;
     const V *vi, *vnext;
     V *w;
     int i;
     double h;
     __device__ __forceinline__ void prepare(const Ctl *c) { h = c->hcol[i]; }
+    template <int W>
     __device__ __forceinline__ void elem(int64_t e, double (&part)[1]) const {
-        const V we = axpy_e(-h, vi[e], w[e]);
-        w[e] = we;
-        part[0] = addd(part[0], mulp(vnext[e], we));
+        const auto VI = ldp<W>(vi, e), VN = ldp<W>(vnext, e);
+        auto Wv = ldp<W>(w, e);
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            Wv.v[k] = axpy_e(-h, VI.v[k], Wv.v[k]);
+            part[0] = addd(part[0], mulp(VN.v[k], Wv.v[k]));
+        }
+        stp<W>(w, e, Wv);
     }
     __device__ __forceinline__ void last(Ctl *c, const double (&tot)[1]) const { c->hcol[i + 1] = tot[0]; }
 };
@@ -103,15 +132,22 @@ __device__ __forceinline__ void givens(double a, double b, double &c, double &s,
 // scalar work: rotations, estimate |g_{j+1}|, criteria, happy breakdown, cycle end
 template <class V>
 struct GmMgsLast : SkipCycleEnd {
+    using value_type = V;
     const V *vj;
     V *w;
     int j;
     double h;
     __device__ __forceinline__ void prepare(const Ctl *c) { h = c->hcol[j]; }
+    template <int W>
     __device__ __forceinline__ void elem(int64_t e, double (&part)[1]) const {
-        const V we = axpy_e(-h, vj[e], w[e]);
-        w[e] = we;
-        part[0] = addd(part[0], mulp(we, we));
+        const auto VJ = ldp<W>(vj, e);
+        auto Wv = ldp<W>(w, e);
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            Wv.v[k] = axpy_e(-h, VJ.v[k], Wv.v[k]);
+            part[0] = addd(part[0], mulp(Wv.v[k], Wv.v[k]));
+        }
+        stp<W>(w, e, Wv);
     }
     __device__ __forceinline__ void last(Ctl *c, const double (&tot)[1]) const {
         double *hc = c->hcol;
@@ -165,11 +201,18 @@ struct GmMgsLast : SkipCycleEnd {
 // v_{j+1} = (1 / ||w||) w
 template <class V>
 struct GmNextBasis : SkipCycleEnd {
+    using value_type = V;
     const V *w;
     V *vn;
     double inv_h;
     __device__ __forceinline__ void prepare(const Ctl *c) { inv_h = 1.0 / c->hnorm; }
-    __device__ __forceinline__ void elem(int64_t e, double (&)[1]) const { vn[e] = scal_e(inv_h, w[e]); }
+    template <int W>
+    __device__ __forceinline__ void elem(int64_t e, double (&)[1]) const {
+        auto Wv = ldp<W>(w, e);
+#pragma unroll
+        for (int k = 0; k < W; ++k) Wv.v[k] = scal_e(inv_h, Wv.v[k]);
+        stp<W>(vn, e, Wv);
+    }
 };
 
 // _back_substitute (solvers.py:301-308)
@@ -190,6 +233,7 @@ struct GmBackSub {
 // x += M zacc; then finish if a criterion fired
 template <class V, int MAXK>
 struct GmUpdate : SkipUnlessCycleEnd {
+    using value_type = V;
     const V *basis;
     size_t vstride;  // elements between consecutive basis vectors
     const V *inv;
@@ -200,11 +244,22 @@ struct GmUpdate : SkipUnlessCycleEnd {
         k = c->k;
         y = c->y;
     }
-    __device__ __forceinline__ void elem(int64_t e, double (&part)[1]) const {
-        V acc = (V)0;
-        for (int i = 0; i < k; ++i) acc = axpy_e(y[i], basis[(size_t)i * vstride + e], acc);
-        x[e] = axpy_e(1.0, precond_e(inv, e, acc), x[e]);
-        (void)part;
+    template <int W>
+    __device__ __forceinline__ void elem(int64_t e, double (&)[1]) const {
+        Pk<V, W> acc;
+#pragma unroll
+        for (int w = 0; w < W; ++w) acc.v[w] = (V)0;
+        for (int i = 0; i < k; ++i) {
+            const auto Vi = ldp<W>(basis + (size_t)i * vstride, e);
+            const double yi = y[i];
+#pragma unroll
+            for (int w = 0; w < W; ++w) acc.v[w] = axpy_e(yi, Vi.v[w], acc.v[w]);
+        }
+        const auto D = ldp_or_one<W>(inv, e);
+        auto X = ldp<W>(x, e);
+#pragma unroll
+        for (int w = 0; w < W; ++w) X.v[w] = axpy_e(1.0, inv ? vmul(acc.v[w], D.v[w]) : acc.v[w], X.v[w]);
+        stp<W>(x, e, X);
     }
     __device__ __forceinline__ void last(Ctl *c, const double (&)[1]) const {
         if (c->finish) finish_with(c, c->iter, c->stop_reason);

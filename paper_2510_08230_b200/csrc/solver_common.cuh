@@ -103,18 +103,67 @@ __device__ __forceinline__ void breakdown(Ctl *c, int64_t it) {
 }
 
 // ---------------------------------------------------------------- elementwise + reduce
-// One grid-stride pass over n rows applying Op::elem, with N fused fp64 reductions
-// finalised (deterministically) in the last block by Op::last.  Fixed grid size.
-inline int solver_grid() { return device_info().sms * 4; }
+// Packs of W consecutive elements moved with one 16-byte (or 8-byte) access; all solver
+// vectors are 16-byte aligned (workspace vectors are 256-byte aligned; b / x / inv are
+// checked by check_solve_args).
+template <class V, int W>
+struct Pk {
+    V v[W];
+};
+template <int W, class V>
+__device__ __forceinline__ Pk<V, W> ldp(const V *p, int64_t i) {
+    Pk<V, W> r;
+    if constexpr (W * sizeof(V) == 16) {
+        const int4 t = *reinterpret_cast<const int4 *>(p + i);
+        memcpy(&r, &t, 16);
+    } else if constexpr (W * sizeof(V) == 8) {
+        const int2 t = *reinterpret_cast<const int2 *>(p + i);
+        memcpy(&r, &t, 8);
+    } else {
+#pragma unroll
+        for (int w = 0; w < W; ++w) r.v[w] = p[i + w];
+    }
+    return r;
+}
+template <int W, class V>
+__device__ __forceinline__ Pk<V, W> ldp_or_one(const V *p, int64_t i) {  // nullptr -> identity
+    if (p) return ldp<W>(p, i);
+    Pk<V, W> r;
+#pragma unroll
+    for (int w = 0; w < W; ++w) r.v[w] = (V)1;
+    return r;
+}
+template <int W, class V>
+__device__ __forceinline__ void stp(V *p, int64_t i, const Pk<V, W> &r) {
+    if constexpr (W * sizeof(V) == 16) {
+        int4 t;
+        memcpy(&t, &r, 16);
+        *reinterpret_cast<int4 *>(p + i) = t;
+    } else if constexpr (W * sizeof(V) == 8) {
+        int2 t;
+        memcpy(&t, &r, 8);
+        *reinterpret_cast<int2 *>(p + i) = t;
+    } else {
+#pragma unroll
+        for (int w = 0; w < W; ++w) p[i + w] = r.v[w];
+    }
+}
 
-template <int N, class Op>
+// One grid-stride pass over n rows in packs of W (tail with W = 1) applying
+// Op::elem<W>, with N fused fp64 reductions finalised (deterministically) in the last
+// block by Op::last.  Fixed grid -> fixed summation order.
+inline int solver_grid() { return device_info().sms * 8; }
+
+template <int N, int W, class Op>
 __global__ void __launch_bounds__(256) ew_kernel(int64_t n, Ctl *ctl, double *partials, Op op) {
     if (loop_done(ctl) || op.skip(ctl)) return;
     op.prepare(ctl);
     double part[N > 0 ? N : 1] = {};
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        op.elem(i, part);
+    const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t npk = n / W;
+    for (int64_t k = gtid; k < npk; k += stride) op.template elem<W>(k * W, part);
+    for (int64_t i = npk * W + gtid; i < n; i += stride) op.template elem<1>(i, part);
     if constexpr (N > 0) {
         double tot[N];
         if (grid_reduce<N>(part, partials, &ctl->ticket[0], tot) && threadIdx.x == 0) op.last(ctl, tot);
@@ -125,7 +174,8 @@ __global__ void __launch_bounds__(256) ew_kernel(int64_t n, Ctl *ctl, double *pa
 
 template <int N, class Op>
 cudaError_t launch_ew(int64_t n, Ctl *ctl, double *partials, const Op &op, cudaStream_t st) {
-    ew_kernel<N, Op><<<solver_grid(), 256, 0, st>>>(n, ctl, partials, op);
+    constexpr int W = 16 / sizeof(typename Op::value_type);
+    ew_kernel<N, W, Op><<<solver_grid(), 256, 0, st>>>(n, ctl, partials, op);
     return cudaGetLastError();
 }
 
@@ -294,6 +344,8 @@ sb_status check_solve_args(const SolveArgs &a, int64_t &n) {
     if (a.b->stride != 1 || a.x->stride != 1)
         return fail(err, SB_ERR_UNSUPPORTED, "solver vectors must be contiguous (stride 1)");
     if (a.crit->max_iters < 1) return fail(err, SB_ERR_INVALID_ARGUMENT, "max_iters must be positive");
+    if (((uintptr_t)a.b->data | (uintptr_t)a.x->data | (uintptr_t)a.inv) % 16 != 0)
+        return fail(err, SB_ERR_UNSUPPORTED, "solver vectors must be 16-byte aligned");
     n = rows;
     return SB_OK;
 }
@@ -336,9 +388,13 @@ inline sb_status finish_log(const Ctl &h, const SolveArgs &a, const SolverWs &w)
 // ================================================================ shared: b.b (bnorm) + residual
 template <class V>
 struct NormB : SkipNone {
+    using value_type = V;
     const V *b;
+    template <int W>
     __device__ __forceinline__ void elem(int64_t i, double (&part)[1]) const {
-        part[0] = addd(part[0], mulp(b[i], b[i]));
+        const auto B = ldp<W>(b, i);
+#pragma unroll
+        for (int w = 0; w < W; ++w) part[0] = addd(part[0], mulp(B.v[w], B.v[w]));
     }
     __device__ __forceinline__ void last(Ctl *c, const double (&tot)[1]) const { c->bnorm = sqrt(tot[0]); }
 };
@@ -357,15 +413,21 @@ __device__ __forceinline__ void exact_log(Ctl *c) {  // solvers.py:179-181
 // first rho = shadow.r equals r.r exactly (same products, same order).
 template <class V>
 struct ShadowInit : SkipNone {
+    using value_type = V;
     const V *b, *t;
     V *r, *shadow;
+    template <int W>
     __device__ __forceinline__ void elem(int64_t i, double (&part)[2]) const {
-        const V bi = b[i];
-        const V ri = axpy_e(-1.0, t[i], bi);
-        r[i] = ri;
-        shadow[i] = ri;
-        part[0] = addd(part[0], mulp(bi, bi));
-        part[1] = addd(part[1], mulp(ri, ri));
+        const auto B = ldp<W>(b, i), T = ldp<W>(t, i);
+        Pk<V, W> R;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            R.v[w] = axpy_e(-1.0, T.v[w], B.v[w]);
+            part[0] = addd(part[0], mulp(B.v[w], B.v[w]));
+            part[1] = addd(part[1], mulp(R.v[w], R.v[w]));
+        }
+        stp<W>(r, i, R);
+        stp<W>(shadow, i, R);
     }
     __device__ __forceinline__ void last(Ctl *c, const double (&tot)[2]) const {
         c->bnorm = sqrt(tot[0]);

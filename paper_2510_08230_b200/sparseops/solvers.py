@@ -193,9 +193,10 @@ class _SolverBase(LinOp):
         else:
             raise UnsupportedFeatureError(
                 f"{type(m).__name__} is not available on the device; use Jacobi or None")
-        # contiguous vectors for the fused kernels (a padded stride is copied around)
-        bb = b if b.stride == 1 else _contiguous_copy(b)
-        xx = x if x.stride == 1 else _contiguous_copy(x)
+        # contiguous, 16-byte aligned vectors for the fused kernels (a padded stride or an
+        # offset view is copied around)
+        bb = b if _packed(b) else _contiguous_copy(b)
+        xx = x if _packed(x) else _contiguous_copy(x)
         crit = _criteria_struct(self.criteria)
         cap = int(min(crit.max_iters, _HISTORY_CAP))
         hist = np.zeros(max(cap, 1), np.float64)
@@ -220,6 +221,10 @@ class _SolverBase(LinOp):
         hl = min(int(log.history_len), cap)
         return ConvergenceLog(int(log.iterations), hist[:hl].tolist(), bool(log.converged),
                               STOP_RESIDUAL if log.stop_reason == 0 else STOP_MAX_ITERS)
+
+
+def _packed(v: DenseMatrix) -> bool:
+    return v.stride == 1 and v.values.data_ptr() % 16 == 0
 
 
 def _contiguous_copy(v: DenseMatrix) -> DenseMatrix:
