@@ -277,14 +277,15 @@ SB_INDEX_DECLS(double, i64)
     sb_status sb_hybrid_tail_ptrs_##IN(int64_t rows, const void *row_ptrs, int64_t width,         \
                                        void *tail_ptrs, int64_t *tail_nnz, sb_stream_t stream,    \
                                        sb_error *err);                                            \
-    /* synthetic stencil generators straight into canonical CSR:                 \
+    /* synthetic stencil generators straight into canonical CSR: rows          \
+       [row_lo, row_hi) (-1 = all) with global columns and row_ptrs relative to row_lo;          \
        dim 2 -> 5-point Poisson, dim 3 -> 7-point with convection c (0 = Poisson) */              \
-    sb_status sb_stencil_csr_double_##IN(int64_t p, int32_t dim, double c, void *row_ptrs,       \
-                                         void *col_idxs, void *values, sb_stream_t stream,        \
-                                         sb_error *err);                                          \
-    sb_status sb_stencil_csr_float_##IN(int64_t p, int32_t dim, double c, void *row_ptrs,        \
-                                        void *col_idxs, void *values, sb_stream_t stream,         \
-                                        sb_error *err);
+    sb_status sb_stencil_csr_double_##IN(int64_t p, int32_t dim, double c, int64_t row_lo,       \
+                                         int64_t row_hi, void *row_ptrs, void *col_idxs,          \
+                                         void *values, sb_stream_t stream, sb_error *err);        \
+    sb_status sb_stencil_csr_float_##IN(int64_t p, int32_t dim, double c, int64_t row_lo,        \
+                                        int64_t row_hi, void *row_ptrs, void *col_idxs,           \
+                                        void *values, sb_stream_t stream, sb_error *err);
 
 SB_IDX_DECLS(i32)
 SB_IDX_DECLS(i64)
@@ -301,6 +302,52 @@ size_t sb_reduce_workspace_bytes(void);
 size_t sb_coo_from_arrays_workspace_bytes(int64_t count);
 size_t sb_solver_workspace_bytes(int32_t solver, int32_t value_bytes, int64_t n, int64_t krylov_dim,
                                  int64_t history_cap);
+
+/* ------------------------------------------------------------------ row-partitioned solves */
+/* One rank's (NCCL) or one partition's (single-GPU loopback) share of a row-partitioned
+ * system: local rows with columns renumbered to [own rows | ghosts],
+ * ghost blocks ordered by owner, and the halo pattern. */
+typedef struct {
+    sb_matrix a;                /* n_local x (n_local + n_ghost), all local rows */
+    int32_t num_views;          /* 0: SpMV after the halo; else views[0] = interior rows (run */
+    int32_t num_neighbors;      /*    while the halo is in flight), views[1..] = the rest    */
+    sb_matrix views[3];
+    int64_t view_row0[3];       /* first local row of each view */
+    int64_t n_local, n_ghost;
+    const int32_t *nbr;         /* host: neighbour ranks / partition indices, ascending */
+    const int64_t *send_count;  /* host, per neighbour */
+    const int64_t *send_lo;     /* host: first local row of a contiguous send block, or -1 */
+    const int64_t *send_off;    /* host: offset into send_idx / send_buf */
+    const int64_t *recv_count;  /* host */
+    const int64_t *recv_off;    /* host: offset inside the ghost region */
+    const void *send_idx;       /* device int64 local rows (non-contiguous neighbours) */
+    void *send_buf;             /* device value buffer (sum of send counts) */
+    const void *inv_diag;       /* device: local Jacobi inverse diagonal, or NULL */
+    sb_dense b, x;              /* local rows (contiguous, 16-byte aligned) */
+    void *workspace;            /* sb_dist_workspace_bytes */
+} sb_dist_part;
+
+/* NCCL (loaded at run time from the process's libnccl.so.2); the unique id is exchanged by
+ * the caller (torch.distributed store). */
+sb_status sb_nccl_unique_id(char out[128], sb_error *err);
+sb_status sb_nccl_comm_init(int32_t nranks, const char id[128], int32_t rank, void **comm,
+                            sb_error *err);
+sb_status sb_nccl_comm_destroy(void *comm, sb_error *err);
+size_t sb_dist_workspace_bytes(int32_t value_bytes, int64_t n_local, int64_t n_ghost,
+                               int64_t history_cap);
+
+/* Row-partitioned Jacobi-CG (solvers.py:188-224 semantics): halo exchange of the search
+ * direction per SpMV (overlapped with the interior rows), fused local dots combined with
+ * ncclAllReduce (comm != NULL, nparts == 1) or summed across `nparts` partitions living
+ * on this one GPU (comm == NULL: the loopback transport that tests the decomposition). */
+#define SB_DIST_DECLS(VN, IN)                                                                    \
+    sb_status sb_dist_cg_solve_##VN##_##IN(sb_dist_part *parts, int32_t nparts, void *comm,       \
+                                           const sb_criteria *crit, sb_log *log,                  \
+                                           sb_stream_t stream, sb_error *err);
+SB_DIST_DECLS(float, i32)
+SB_DIST_DECLS(float, i64)
+SB_DIST_DECLS(double, i32)
+SB_DIST_DECLS(double, i64)
 
 /* solver ids for sb_solver_workspace_bytes */
 enum { SB_SOLVER_CG = 0, SB_SOLVER_CGS = 1, SB_SOLVER_GMRES = 2, SB_SOLVER_BICGSTAB = 3 };

@@ -23,9 +23,22 @@ LIB = os.path.join(PKG, "libsparseb200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+def _nccl_include():
+    """nccl.h from the NCCL wheel torch ships with (types only; NCCL is dlopen'ed)."""
+    try:
+        import nvidia.nccl
+        for base in nvidia.nccl.__path__:
+            inc = os.path.join(base, "include")
+            if os.path.exists(os.path.join(inc, "nccl.h")):
+                return inc
+    except ImportError:
+        pass
+    return "/usr/include"
+
+
 FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-fvisibility=hidden", "-I", os.path.join(REPO, "include"),
-         "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+         "-I", _nccl_include(), "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 
 
 def _headers():
@@ -60,7 +73,7 @@ def build(verbose: bool = True) -> str:
         raise RuntimeError("nvcc failed:\n" + "\n".join(errors))
     objs = [o for o, _ in results]
     if _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -93,6 +93,16 @@ class SbLog(ctypes.Structure):
                 ("history_cap", c_i64)]
 
 
+class SbDistPart(ctypes.Structure):
+    _fields_ = [("a", SbMatrix), ("num_views", c_i32), ("num_neighbors", c_i32),
+                ("views", SbMatrix * 3), ("view_row0", c_i64 * 3), ("n_local", c_i64),
+                ("n_ghost", c_i64), ("nbr", ctypes.POINTER(c_i32)),
+                ("send_count", ctypes.POINTER(c_i64)), ("send_lo", ctypes.POINTER(c_i64)),
+                ("send_off", ctypes.POINTER(c_i64)), ("recv_count", ctypes.POINTER(c_i64)),
+                ("recv_off", ctypes.POINTER(c_i64)), ("send_idx", c_vp), ("send_buf", c_vp),
+                ("inv_diag", c_vp), ("b", SbDense), ("x", SbDense), ("workspace", c_vp)]
+
+
 FMT_CSR, FMT_COO, FMT_ELL, FMT_SELLP, FMT_HYBRID = 0, 1, 2, 3, 4
 CSR_AUTO, CSR_STRICT, CSR_STREAM, CSR_VECTOR, CSR_MERGE = 0, 1, 2, 3, 4
 CSR_KERNELS = {"auto": CSR_AUTO, "strict": CSR_STRICT, "stream": CSR_STREAM,
@@ -134,6 +144,8 @@ _VI_PROTOS = {
     "sb_bicgstab_solve_{v}_{i}": (c_i32, _SOLVE),
     "sb_gmres_solve_{v}_{i}": (c_i32, [P(SbMatrix), c_vp, P(SbDense), P(SbDense), P(SbCriteria),
                                        c_i64, c_vp, P(SbLog), c_vp, P(SbError)]),
+    "sb_dist_cg_solve_{v}_{i}": (c_i32, [P(SbDistPart), c_i32, c_vp, P(SbCriteria), P(SbLog),
+                                         c_vp, P(SbError)]),
 }
 _I_PROTOS = {
     "sb_csr_row_stats_{i}": (c_i32, [c_i64, c_vp, c_vp, P(SbRowStats), c_vp, P(SbError)]),
@@ -142,10 +154,10 @@ _I_PROTOS = {
     "sb_coo_row_idxs_from_csr_{i}": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_vp, P(SbError)]),
     "sb_sellp_slices_{i}": (c_i32, [c_i64, c_vp, c_i64, c_vp, c_vp, P(c_i64), c_vp, P(SbError)]),
     "sb_hybrid_tail_ptrs_{i}": (c_i32, [c_i64, c_vp, c_i64, c_vp, P(c_i64), c_vp, P(SbError)]),
-    "sb_stencil_csr_double_{i}": (c_i32, [c_i64, c_i32, c_f64, c_vp, c_vp, c_vp, c_vp,
-                                          P(SbError)]),
-    "sb_stencil_csr_float_{i}": (c_i32, [c_i64, c_i32, c_f64, c_vp, c_vp, c_vp, c_vp,
-                                         P(SbError)]),
+    "sb_stencil_csr_double_{i}": (c_i32, [c_i64, c_i32, c_f64, c_i64, c_i64, c_vp, c_vp, c_vp,
+                                          c_vp, P(SbError)]),
+    "sb_stencil_csr_float_{i}": (c_i32, [c_i64, c_i32, c_f64, c_i64, c_i64, c_vp, c_vp, c_vp,
+                                         c_vp, P(SbError)]),
 }
 _PLAIN_PROTOS = {
     "sb_version": (c_i32, []),
@@ -157,6 +169,10 @@ _PLAIN_PROTOS = {
     "sb_reduce_workspace_bytes": (c_sz, []),
     "sb_coo_from_arrays_workspace_bytes": (c_sz, [c_i64]),
     "sb_solver_workspace_bytes": (c_sz, [c_i32, c_i32, c_i64, c_i64, c_i64]),
+    "sb_nccl_unique_id": (c_i32, [ctypes.c_char_p, P(SbError)]),
+    "sb_nccl_comm_init": (c_i32, [c_i32, ctypes.c_char_p, c_i32, P(c_vp), P(SbError)]),
+    "sb_nccl_comm_destroy": (c_i32, [c_vp, P(SbError)]),
+    "sb_dist_workspace_bytes": (c_sz, [c_i32, c_i64, c_i64, c_i64]),
 }
 
 

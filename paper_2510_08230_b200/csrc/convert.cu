@@ -195,16 +195,22 @@ __device__ __forceinline__ int64_t count_eq(int64_t i, int64_t s, int64_t p, int
 }
 
 template <class V, class I>
-__global__ void stencil_kernel(int64_t p, int dim, double c, I *rp, I *ci, V *val) {
-    const int64_t n = dim == 2 ? p * p : p * p * p;
+__global__ void stencil_kernel(int64_t p, int dim, double c, int64_t lo, int64_t hi, I *rp, I *ci,
+                               V *val) {
+    // rows [lo, hi) of the global stencil; row_ptrs relative to row lo, columns global
     const double lo_v = -1.0 - c / 2.0, hi_v = -1.0 + c / 2.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t start = (2 * dim + 1) * i;
+    auto start_of = [&](int64_t i) {
+        int64_t st = (2 * dim + 1) * i;
         int64_t s = 1;
-        for (int d = 0; d < dim; ++d, s *= p) start -= count_eq(i, s, p, 0) + count_eq(i, s, p, p - 1);
-        rp[i] = (I)start;
-        if (i == n) continue;
+        for (int d = 0; d < dim; ++d, s *= p) st -= count_eq(i, s, p, 0) + count_eq(i, s, p, p - 1);
+        return st;
+    };
+    const int64_t base = start_of(lo);
+    for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= hi;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t start = start_of(i) - base;
+        rp[i - lo] = (I)start;
+        if (i == hi) continue;
         int64_t g[3] = {i % p, (i / p) % p, dim == 3 ? i / (p * p) : 0};
         int64_t strides[3] = {1, p, p * p};
         int64_t k = start;
@@ -465,11 +471,14 @@ sb_status hybrid_tail_ptrs(int64_t rows, const void *rp, int64_t width, void *ta
 }
 
 template <class V, class I>
-sb_status stencil(int64_t p, int dim, double c, void *rp, void *ci, void *val, cudaStream_t st,
-                  sb_error *err) {
+sb_status stencil(int64_t p, int dim, double c, int64_t lo, int64_t hi, void *rp, void *ci, void *val,
+                  cudaStream_t st, sb_error *err) {
     if (p < 1 || (dim != 2 && dim != 3)) return fail(err, SB_ERR_INVALID_ARGUMENT, "stencil: p >= 1, dim in {2, 3}");
     const int64_t n = dim == 2 ? p * p : p * p * p;
-    stencil_kernel<V, I><<<elem_grid(n + 1), 256, 0, st>>>(p, dim, c, (I *)rp, (I *)ci, (V *)val);
+    if (lo < 0) lo = 0;
+    if (hi < 0 || hi > n) hi = n;
+    if (lo > hi) return fail(err, SB_ERR_INVALID_ARGUMENT, "stencil: empty row range");
+    stencil_kernel<V, I><<<elem_grid(hi - lo + 1), 256, 0, st>>>(p, dim, c, lo, hi, (I *)rp, (I *)ci, (V *)val);
     SB_CUDA(cudaGetLastError());
     return SB_OK;
 }
@@ -518,18 +527,22 @@ size_t sb_coo_from_arrays_workspace_bytes(int64_t count) { return canon_bytes(co
                                    err);                                                           \
         SB_GUARD_END                                                                               \
     }                                                                                              \
-    sb_status sb_stencil_csr_double_##IN(int64_t p, int32_t dim, double c, void *row_ptrs,        \
+    sb_status sb_stencil_csr_double_##IN(int64_t p, int32_t dim, double c, int64_t row_lo,       \
+                                         int64_t row_hi, void *row_ptrs,                           \
                                          void *col_idxs, void *values, sb_stream_t stream,         \
                                          sb_error *err) {                                          \
         SB_GUARD_BEGIN                                                                             \
-        return stencil<double, I>(p, dim, c, row_ptrs, col_idxs, values, as_stream(stream), err);  \
+        return stencil<double, I>(p, dim, c, row_lo, row_hi, row_ptrs, col_idxs, values,           \
+                                  as_stream(stream), err);                                         \
         SB_GUARD_END                                                                               \
     }                                                                                              \
-    sb_status sb_stencil_csr_float_##IN(int64_t p, int32_t dim, double c, void *row_ptrs,         \
+    sb_status sb_stencil_csr_float_##IN(int64_t p, int32_t dim, double c, int64_t row_lo,        \
+                                        int64_t row_hi, void *row_ptrs,                            \
                                         void *col_idxs, void *values, sb_stream_t stream,          \
                                         sb_error *err) {                                           \
         SB_GUARD_BEGIN                                                                             \
-        return stencil<float, I>(p, dim, c, row_ptrs, col_idxs, values, as_stream(stream), err);   \
+        return stencil<float, I>(p, dim, c, row_lo, row_hi, row_ptrs, col_idxs, values,            \
+                                 as_stream(stream), err);                                          \
         SB_GUARD_END                                                                               \
     }
 

@@ -55,6 +55,7 @@ struct Ctl {
     double *hcol, *g, *cs, *sn, *y, *R;  // R: dim x dim, row-major
     double hnorm, beta_restart;
     int64_t cycle;
+    double dot[8];  // row-partitioned solves: local dot totals, reduced across ranks in place
 };
 
 __device__ __forceinline__ void stop_loop(Ctl *c) {
