@@ -15,8 +15,11 @@ against the measured HBM copy bandwidth in MEASURED_PEAKS.json.  `cpu_baseline` 
 the oracle port (oracle/sbref.cpp) of the reference's CG on this host's cores for a
 bounded sample of iterations.
 
-Multi-GPU (torchrun, N > 1): each rank runs the same single-GPU solve (replicas;
-the row-partitioned NCCL solver is reported separately by bench_dist.py).
+Multi-GPU (torchrun, N > 1): the SAME global system is row-partitioned across the N
+GPUs (paper_2510_08230_b200.dist: NCCL halo exchange overlapped with the interior
+SpMV, ncclAllReduce of the fused dots) -> strong scaling; `value` stays global CG
+iterations per second.  `--workload cg512` selects BASELINE config #5 (Poisson 512^3,
+134M rows), the north_star strong-scaling problem.
 """
 
 from __future__ import annotations
@@ -33,6 +36,7 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 METRIC = "SpMV GB/s & % HBM roofline; CG solve time/iters/s, Poisson-3D fp64, 1/2/4/8 GPU"
+WORKLOADS = {"cg128": 128, "cg512": 512}
 P = 128
 RTOL = 1e-8
 
@@ -154,7 +158,7 @@ def run_reference(args):
     v = statistics.median(vals)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "CG iters/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 30 * 1000.0 / v, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 30 * 1000.0 / v, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "Jacobi-CG fp64 3-D 7-pt Poisson 128^3, rtol 1e-8 "
                                    "(fixed-iteration CPU sample of 30 iterations per step)"},
@@ -167,23 +171,55 @@ def run_reference(args):
         dist.barrier()
 
 
+def _spmv_roofline(a, dev, stream, torch, sp):
+    """Average CUDA-event duration of the dominant kernel (the CSR SpMV of the iteration)
+    over 50 back-to-back launches on the solver's stream."""
+    n, nnz = a.rows, a.nnz
+    p_vec = sp.dense_create(dev, a.cols, 1, sp.Precision.double, 1.0)
+    q_vec = sp.dense_create(dev, n, 1, sp.Precision.double, 0.0)
+    for _ in range(5):
+        a.apply(p_vec, q_vec)
+    reps = 50
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    s0.record(stream)
+    for _ in range(reps):
+        a.apply(p_vec, q_vec)
+    s1.record(stream)
+    torch.cuda.synchronize()
+    spmv_ms = s0.elapsed_time(s1) / reps
+    spmv_bytes = a.precision.itemsize * (nnz + n + a.cols) + a.index_width.itemsize * (nnz + n + 1)
+    peak, peak_kind = _peaks()
+    achieved = spmv_bytes / (spmv_ms / 1e3) / 1e9
+    return spmv_ms, spmv_bytes, {
+        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+        "traffic": None, "kernel": f"csr_{a.kernel}_kernel<double,int>",
+        "alg_bytes_per_launch": spmv_bytes, "peak_source": peak_kind}
+
+
 def run_ours(args):
-    import numpy as np
     import torch
 
     world, rank, local = _dist()
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.partitioned:
         import torch.distributed as dist
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return run_partitioned(args, world, rank, local)
 
     from paper_2510_08230_b200 import gen
     from paper_2510_08230_b200 import pysparseops as pg
     from paper_2510_08230_b200 import sparseops as sp
 
+    p = WORKLOADS[args.workload]
     dev = sp.create_device("cuda", local)
     stream = torch.cuda.current_stream()
-    a = gen.poisson3d(dev, P)
+    a = gen.poisson3d(dev, p)
     n, nnz = a.rows, a.nnz
     m = sp.jacobi_create(a)
     solver = sp.Cg(a, criteria=[sp.Iteration(100000), sp.ResidualNorm(RTOL)], preconditioner=m)
@@ -197,7 +233,6 @@ def run_ours(args):
     for _ in range(max(args.warmup, 1)):
         log = step()
     torch.cuda.synchronize()
-    _barrier(world)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     iters = 0
     with ClockSampler(local) as clocks:
@@ -208,28 +243,10 @@ def run_ours(args):
         ev1.record(stream)
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
-    ms_max = _max_over_ranks(ms, world)
-    _barrier(world)
-    total_iters = iters * world
-    value = total_iters / (ms_max / 1000.0)
+    value = iters / (ms / 1000.0)
 
-    # ---- dominant kernel: the CSR SpMV, timed live with CUDA events on its stream
-    p_vec = sp.dense_create(dev, n, 1, sp.Precision.double, 1.0)
-    q_vec = sp.dense_create(dev, n, 1, sp.Precision.double, 0.0)
-    for _ in range(5):
-        a.apply(p_vec, q_vec)
-    reps = 50
-    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    s0.record(stream)
-    for _ in range(reps):
-        a.apply(p_vec, q_vec)
-    s1.record(stream)
-    torch.cuda.synchronize()
-    spmv_ms = s0.elapsed_time(s1) / reps
-    spmv_bytes = 12 * nnz + 4 * (n + 1) + 8 * n + 8 * n
-    peak, peak_kind = _peaks()
-    achieved = spmv_bytes / (spmv_ms / 1e3) / 1e9
+    spmv_ms, spmv_bytes, roofline = _spmv_roofline(a, dev, stream, torch, sp)
+    peak = roofline["peak"]
     cg_iter_bytes = (12 * nnz + 4 * (n + 1)) + 13 * 8 * n
     cg_iter_ms = ms / max(iters, 1)
 
@@ -251,7 +268,99 @@ def run_ours(args):
     for _ in range(max(args.warmup, 1)):
         e2e_step()
     torch.cuda.synchronize()
-    _barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_iters = 0
+    e0.record(stream)
+    for _ in range(args.steps):
+        e_iters += e2e_step().iterations
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_value = e_iters / (e0.elapsed_time(e1) / 1e3)
+    assert abs(float(xh[n // 2]) - float(x.values[n // 2])) <= 1e-6 * abs(float(x.values[n // 2]))
+
+    cpu = cpu_baseline_sample() if not args.no_cpu and p == 128 else None
+    line = {
+        "metric": METRIC, "value": value, "unit": "CG iters/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (device-generated 7-point Poisson stencil, b = 1, x0 = 0)",
+        "config": {"workload": f"Jacobi-CG fp64 3-D 7-pt Poisson {p}^3 (n={n:,}, nnz={nnz:,}), "
+                               f"rtol 1e-8, CSR",
+                   "parallelism": "single GPU",
+                   "l2": "inputs larger than L2 (CG working set >= 284 MB vs 126 MB L2); no flush"},
+        "iterations_per_solve": log.iterations,
+        "solve_ms": ms / args.steps,
+        "cg_iteration": {"ms": cg_iter_ms, "alg_bytes": cg_iter_bytes,
+                         "gbs": cg_iter_bytes / (cg_iter_ms / 1e3) / 1e9,
+                         "frac_of_hbm": cg_iter_bytes / (cg_iter_ms / 1e3) / 1e9 / peak},
+        "spmv": {"kernel": a.kernel, "us": spmv_ms * 1e3, "gbs": roofline["achieved"],
+                 "gflops": 2 * nnz / (spmv_ms / 1e3) / 1e9},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "CG iters/s", "h2d_bytes_per_step": 2 * 8 * n,
+                "d2h_bytes_per_step": 8 * n + 64},
+        "gpu_launches": args.steps * (2 + 3 * log.iterations),
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line))
+
+
+def run_partitioned(args, world, rank, local):
+    """Strong scaling: the same global Poisson system row-partitioned over `world` GPUs."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_08230_b200 import dist as D
+    from paper_2510_08230_b200 import sparseops as sp
+
+    p = WORKLOADS[args.workload]
+    dev = sp.create_device("cuda", local)
+    stream = torch.cuda.current_stream()
+    comm = D.NcclComm(rank, world)
+    part = D.stencil_partition(dev, p, rank, world)
+    nl = part.n_local
+    solver = D.DistCg(part, [sp.Iteration(100000), sp.ResidualNorm(RTOL)], comm=comm)
+    b = sp.dense_create(dev, nl, 1, sp.Precision.double, 1.0)
+    x = sp.dense_create(dev, nl, 1, sp.Precision.double, 0.0)
+
+    def step():
+        x.values.zero_()
+        return solver.solve(b, x)
+
+    for _ in range(max(args.warmup, 1)):
+        log = step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = 0
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            log = step()
+            iters += log.iterations
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = _max_over_ranks(ev0.elapsed_time(ev1), world)
+    dist.barrier()
+    value = iters / (ms / 1000.0)  # global system: iterations are not multiplied by ranks
+
+    _, _, roofline = _spmv_roofline(part.matrix, dev, stream, torch, sp)
+
+    # e2e: host slabs of b and x0 -> device, solve, x slab back
+    bh = torch.ones(nl, dtype=torch.float64).pin_memory()
+    x0h = torch.zeros(nl, dtype=torch.float64).pin_memory()
+    xh = torch.empty(nl, dtype=torch.float64).pin_memory()
+
+    def e2e_step():
+        bt = sp.dense_from_array(dev, bh.to(dev.torch, non_blocking=True))
+        xt = sp.dense_from_array(dev, x0h.to(dev.torch, non_blocking=True))
+        lg = solver.solve(bt, xt)
+        xh.copy_(xt.values, non_blocking=True)
+        return lg
+
+    e2e_step()
+    torch.cuda.synchronize()
+    dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e_iters = 0
     e0.record(stream)
@@ -260,43 +369,28 @@ def run_ours(args):
     e1.record(stream)
     torch.cuda.synchronize()
     e_ms = _max_over_ranks(e0.elapsed_time(e1), world)
-    e2e_value = e_iters * world / (e_ms / 1e3)
-    assert abs(float(xh[n // 2]) - float(x.values[n // 2])) <= 1e-6 * abs(float(x.values[n // 2]))
-
-    if rank != 0:
-        if world > 1:
-            torch.distributed.destroy_process_group()
-        return
-    cpu = cpu_baseline_sample() if not args.no_cpu else None
-    line = {
-        "metric": METRIC, "value": value, "unit": "CG iters/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (device-generated 7-point Poisson stencil, b = 1, x0 = 0)",
-        "config": {"workload": "Jacobi-CG fp64 3-D 7-pt Poisson 128^3 (n=2,097,152, "
-                               "nnz=14,581,760), rtol 1e-8, CSR",
-                   "parallelism": "replicas" if world > 1 else "single",
-                   "l2": "inputs larger than L2 (CG working set 284 MB vs 126 MB L2); no flush"},
-        "iterations_per_solve": log.iterations,
-        "solve_ms": ms / args.steps,
-        "cg_iteration": {"ms": cg_iter_ms, "alg_bytes": cg_iter_bytes,
-                         "gbs": cg_iter_bytes / (cg_iter_ms / 1e3) / 1e9,
-                         "frac_of_hbm": cg_iter_bytes / (cg_iter_ms / 1e3) / 1e9 / peak},
-        "spmv": {"kernel": a.kernel, "us": spmv_ms * 1e3, "gbs": achieved,
-                 "gflops": 2 * nnz / (spmv_ms / 1e3) / 1e9},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
-                     "kernel": f"csr_{a.kernel}_kernel<double,int>",
-                     "alg_bytes_per_launch": spmv_bytes, "peak_source": peak_kind},
-        "cpu_baseline": cpu,
-        "e2e": {"value": e2e_value, "unit": "CG iters/s", "h2d_bytes_per_step": 2 * 8 * n,
-                "d2h_bytes_per_step": 8 * n + 64},
-        "gpu_launches": args.steps * (2 + 3 * log.iterations),
-        "clocks": clocks.summary(),
-    }
-    print(json.dumps(line))
-    if world > 1:
-        torch.distributed.destroy_process_group()
+    comm.close()
+    if rank == 0:
+        n = p ** 3
+        line = {
+            "metric": METRIC, "value": value, "unit": "CG iters/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (device-generated 7-point Poisson stencil slabs, b = 1, x0 = 0)",
+            "config": {"workload": f"row-partitioned Jacobi-CG fp64 3-D 7-pt Poisson {p}^3 "
+                                   f"(n={n:,}), rtol 1e-8, CSR slabs",
+                       "parallelism": f"row partition over {world} GPUs, NCCL halo + allreduce",
+                       "l2": "inputs larger than L2 per rank at 512^3; no flush"},
+            "iterations_per_solve": log.iterations, "solve_ms": ms / args.steps,
+            "roofline": roofline, "cpu_baseline": None,
+            "e2e": {"value": e_iters / (e_ms / 1e3), "unit": "CG iters/s",
+                    "h2d_bytes_per_step": 2 * 8 * nl, "d2h_bytes_per_step": 8 * nl},
+            "gpu_launches": args.steps * (6 + 8 * log.iterations),
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line))
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 def main():
@@ -306,6 +400,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="use the row-partitioned NCCL solver even on one GPU")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cg128",
+                    help="cg128 = BASELINE config #2 (default); cg512 = config #5")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
