@@ -95,7 +95,7 @@ typedef struct {
     int32_t kernel;         /* SB_CSR_* */
     int32_t block_rows;     /* stream: rows per block R; vector: lanes per row */
     int32_t nnz_cap;        /* stream: max nnz of one R-row block */
-    int32_t pad;
+    int32_t nnz_cap256;     /* stream: max nnz of one 256-row block (solver epilogues) */
     int64_t num_tiles;      /* merge: tiles of items_per_tile merge items */
     int64_t items_per_tile;
     void *tile_rows;        /* merge: int64[num_tiles + 1] */

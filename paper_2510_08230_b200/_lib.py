@@ -14,7 +14,7 @@ import threading
 from .sparseops import errors as E
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsparseb200.so")
+LIB_PATH = os.environ.get("SPARSEB200_LIB") or os.path.join(_HERE, "libsparseb200.so")
 
 c_i32 = ctypes.c_int32
 c_i64 = ctypes.c_int64
@@ -44,7 +44,7 @@ class SbRowStats(ctypes.Structure):
 
 
 class SbCsrPlan(ctypes.Structure):
-    _fields_ = [("kernel", c_i32), ("block_rows", c_i32), ("nnz_cap", c_i32), ("pad", c_i32),
+    _fields_ = [("kernel", c_i32), ("block_rows", c_i32), ("nnz_cap", c_i32), ("nnz_cap256", c_i32),
                 ("num_tiles", c_i64), ("items_per_tile", c_i64), ("tile_rows", c_vp),
                 ("tile_nnz", c_vp), ("carry_rows", c_vp), ("carry_vals", c_vp)]
 

@@ -97,8 +97,10 @@ sb_status plan_select(const sb_row_stats *S, int vbytes, int ibytes, int force, 
     int kernel = force;
     // stream feasibility: two stages of one R-row block must fit comfortably in smem
     int stream_R = 0, stream_cap = 0;
-    const int Rs[3] = {256, 128, 64};
-    const int qidx[3] = {3, 2, 1};
+    // 128-row blocks first: best measured (0.946 / 0.967 of the copy peak at 128^3 / 256^3,
+    // tools/tune_stream.py) -- finer tail balance at 8 CTAs of smem per SM
+    const int Rs[3] = {128, 256, 64};
+    const int qidx[3] = {2, 3, 1};
     for (int t = 0; t < 3; ++t) {
         const int64_t cap = S->max_block_nnz[qidx[t]];
         const size_t bytes = 2 * ((size_t)(cap + 16) * (vbytes + ibytes) + (size_t)(Rs[t] + 16) * ibytes);
@@ -123,6 +125,9 @@ sb_status plan_select(const sb_row_stats *S, int vbytes, int ibytes, int force, 
     if (kernel == SB_CSR_STREAM) {
         P->block_rows = stream_R;
         P->nnz_cap = stream_cap;
+        const int64_t cap256 = S->max_block_nnz[3];
+        const size_t bytes256 = 2 * ((size_t)(cap256 + 16) * (vbytes + ibytes) + (size_t)(256 + 16) * ibytes);
+        P->nnz_cap256 = (cap256 < (1 << 30) && bytes256 <= 96 * 1024) ? (int)std::max<int64_t>(cap256, 1) : 0;
     } else if (kernel == SB_CSR_VECTOR) {
         int lanes = 2;
         while (lanes < 32 && lanes < mean / 2.0) lanes <<= 1;

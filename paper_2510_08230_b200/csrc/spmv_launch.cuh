@@ -130,6 +130,17 @@ cudaError_t csr_apply(const sb_csr &A, const V *b, int64_t ldb, V *x_out, int64_
     int kernel = P ? P->kernel : SB_CSR_STRICT;
     if (A.rows == 0) return cudaSuccess;
     if (kernel == SB_CSR_STREAM) {
+        // plain SpMV: 128-row blocks (0.95 of the copy peak, tools/tune_stream.py); fused
+        // solver epilogues keep 256-row blocks (fewer, longer blocks hide the epilogue's own
+        // loads; measured best for the CG iteration, tools/cg_ab.py).  A 256-row block holds
+        // at most twice the nnz of a 128-row block.
+        if (!is_plain_store<Epi>::value && P->block_rows == 128 && P->nnz_cap256 > 0) {
+            sb_csr_plan P2 = *P;
+            P2.nnz_cap = P->nnz_cap256;
+            sb_csr A2 = A;
+            A2.plan = &P2;
+            return launch_csr_stream<V, I, 256>(A2, b, ldb, epi, st);
+        }
         if (P->block_rows == 256) return launch_csr_stream<V, I, 256>(A, b, ldb, epi, st);
         if (P->block_rows == 128) return launch_csr_stream<V, I, 128>(A, b, ldb, epi, st);
         return launch_csr_stream<V, I, 64>(A, b, ldb, epi, st);
