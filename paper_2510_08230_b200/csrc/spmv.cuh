@@ -219,7 +219,21 @@ __global__ void __launch_bounds__(256) csr_vector_kernel(int64_t rows, const I *
         double acc = 0.0;
         if (i < rows) {
             const int64_t kb = rp[i], ke = rp[i + 1];
-            for (int64_t k = kb + lane; k < ke; k += S)
+            int64_t k = kb + lane;
+            for (; k + 3 * S < ke; k += 4 * S) {  // four independent gathers in flight
+                I c[4];
+                V v[4], g[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    c[u] = ld_stream(ci + k + u * S);
+                    v[u] = ld_stream(val + k + u * S);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) g[u] = __ldg(b + (int64_t)c[u] * ldb);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) acc = addd(acc, mulp(v[u], g[u]));
+            }
+            for (; k < ke; k += S)
                 acc = addd(acc, mulp(ld_stream(val + k), __ldg(b + (int64_t)ld_stream(ci + k) * ldb)));
         }
 #pragma unroll
@@ -284,6 +298,35 @@ __device__ __forceinline__ void scan_by_key(int64_t &key, double &val, int64_t &
     __syncthreads();  // s_k / s_v reusable by the next call
 }
 
+// Products of a tile's nonzeros into shared memory with every load of a thread issued
+// before any is used: IPT coalesced (col, val) pairs, then IPT independent gathers of b
+// (the random gathers of irregular matrices are latency-bound without this MLP).
+template <class V, class I, int NT, int IPT>
+__device__ __forceinline__ void stage_products(const I *__restrict__ ci, const V *__restrict__ val,
+                                               int64_t count, const V *__restrict__ b, int64_t ldb,
+                                               double *s_prod) {
+    I cc[IPT];
+    V vv[IPT], bb[IPT];
+#pragma unroll
+    for (int u = 0; u < IPT; ++u) {
+        const int64_t j = threadIdx.x + (int64_t)u * NT;
+        if (j < count) {
+            cc[u] = ld_stream(ci + j);
+            vv[u] = ld_stream(val + j);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < IPT; ++u) {
+        const int64_t j = threadIdx.x + (int64_t)u * NT;
+        if (j < count) bb[u] = __ldg(b + (int64_t)cc[u] * ldb);
+    }
+#pragma unroll
+    for (int u = 0; u < IPT; ++u) {
+        const int64_t j = threadIdx.x + (int64_t)u * NT;
+        if (j < count) s_prod[j] = mulp(vv[u], bb[u]);
+    }
+}
+
 // ============================================================ CSR: merge-path
 // Load-balanced: every tile owns exactly NT*IPT merge items (row ends + nonzeros),
 // so a CTA's work is independent of the row-length distribution.  Tile start
@@ -337,10 +380,7 @@ __global__ void __launch_bounds__(NT) csr_merge_kernel(int64_t rows, const I *__
         const int64_t nA = row_e - row_s, nB = k_e - k_s;
         const int64_t nload = (row_e + 1 < rows ? row_e + 1 : rows) - row_s;  // ends of rows row_s..row_e
         for (int64_t j = threadIdx.x; j < nload; j += NT) s_end[j] = rp[row_s + j + 1];
-        for (int64_t j = threadIdx.x; j < nB; j += NT) {
-            const int64_t k = k_s + j;
-            s_prod[j] = mulp(ld_stream(val + k), __ldg(b + (int64_t)ld_stream(ci + k) * ldb));
-        }
+        stage_products<V, I, NT, IPT>(ci + k_s, val + k_s, nB, b, ldb, s_prod);
         __syncthreads();
         const int64_t total = nA + nB;
         const int64_t d0 = (int64_t)threadIdx.x * IPT;
@@ -419,11 +459,8 @@ __global__ void __launch_bounds__(NT) coo_kernel(int64_t rows, int64_t nnz, cons
         const int64_t e0 = tile * TILE;
         const int64_t e1 = e0 + TILE < nnz ? e0 + TILE : nnz;
         const int64_t ne = e1 - e0;
-        for (int64_t j = threadIdx.x; j < ne; j += NT) {
-            const int64_t e = e0 + j;
-            s_key[j] = (int64_t)ld_stream(ri + e);
-            s_prod[j] = mulp(ld_stream(val + e), __ldg(b + (int64_t)ld_stream(ci + e) * ldb));
-        }
+        for (int64_t j = threadIdx.x; j < ne; j += NT) s_key[j] = (int64_t)ld_stream(ri + e0 + j);
+        stage_products<V, I, NT, IPT>(ci + e0, val + e0, ne, b, ldb, s_prod);
         if (threadIdx.x == 0) s_key[ne] = e1 < nnz ? (int64_t)ri[e1] : INT64_MAX;
         __syncthreads();
         if (!accumulate) {
@@ -475,6 +512,63 @@ __global__ void __launch_bounds__(NT) coo_kernel(int64_t rows, int64_t nnz, cons
     }
 }
 
+// ============================================================ padded layouts (ELL / SELL-P)
+// One column of RPT consecutive rows: 16-byte value vector and 8/16-byte index vector.
+template <class V, class I, int RPT>
+__device__ __forceinline__ void load_column(const V *__restrict__ val, const I *__restrict__ col,
+                                            int64_t base, V (&vv)[RPT], I (&cc)[RPT]) {
+    if constexpr (RPT * sizeof(V) == 16) {
+        int4 raw = __ldcs(reinterpret_cast<const int4 *>(val + base));
+        memcpy(vv, &raw, 16);
+    } else {
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) vv[r] = __ldcs(val + base + r);
+    }
+    if constexpr (RPT * sizeof(I) == 16) {
+        int4 raw = __ldcs(reinterpret_cast<const int4 *>(col + base));
+        memcpy(cc, &raw, 16);
+    } else if constexpr (RPT * sizeof(I) == 8) {
+        int2 raw = __ldcs(reinterpret_cast<const int2 *>(col + base));
+        memcpy(cc, &raw, 8);
+    } else {
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) cc[r] = __ldcs(col + base + r);
+    }
+}
+
+// Accumulate `len` padded columns (column k at base0 + k*kstride) for RPT rows, four
+// columns per step with all loads and gathers issued before the ordered adds (padding
+// col = -1 is skipped, so each row's sum keeps the CSR order exactly).
+template <class V, class I, int RPT>
+__device__ __forceinline__ void padded_rows(const V *__restrict__ val, const I *__restrict__ col,
+                                            const V *__restrict__ b, int64_t ldb, int64_t base0,
+                                            int64_t kstride, int64_t len, double (&acc)[RPT]) {
+    int64_t k = 0;
+    for (; k + 4 <= len; k += 4) {
+        V vv[4][RPT], gg[4][RPT];
+        I cc[4][RPT];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) load_column<V, I, RPT>(val, col, base0 + (k + u) * kstride, vv[u], cc[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) gg[u][r] = cc[u][r] >= 0 ? __ldg(b + (int64_t)cc[u][r] * ldb) : (V)0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int r = 0; r < RPT; ++r)
+                if (cc[u][r] >= 0) acc[r] = addd(acc[r], mulp(vv[u][r], gg[u][r]));
+    }
+    for (; k < len; ++k) {
+        V vv[RPT];
+        I cc[RPT];
+        load_column<V, I, RPT>(val, col, base0 + k * kstride, vv, cc);
+#pragma unroll
+        for (int r = 0; r < RPT; ++r)
+            if (cc[r] >= 0) acc[r] = addd(acc[r], mulp(vv[r], __ldg(b + (int64_t)cc[r] * ldb)));
+    }
+}
+
 // ============================================================ ELL (column-major)
 // RPT consecutive rows per thread with 16-byte vector loads of values (and 8/16-byte
 // loads of column indices); per-row order is the stored order -> bitwise = reference.
@@ -491,31 +585,7 @@ __global__ void __launch_bounds__(256) ell_kernel(int64_t rows, int64_t width, i
         double acc[RPT];
 #pragma unroll
         for (int r = 0; r < RPT; ++r) acc[r] = 0.0;
-        for (int64_t k = 0; k < width; ++k) {
-            const int64_t base = k * stride + i0;
-            V vv[RPT];
-            I cc[RPT];
-            if constexpr (RPT * sizeof(V) == 16) {
-                int4 raw = __ldcs(reinterpret_cast<const int4 *>(val + base));
-                memcpy(vv, &raw, 16);
-            } else {
-#pragma unroll
-                for (int r = 0; r < RPT; ++r) vv[r] = __ldcs(val + base + r);
-            }
-            if constexpr (RPT * sizeof(I) == 16) {
-                int4 raw = __ldcs(reinterpret_cast<const int4 *>(col + base));
-                memcpy(cc, &raw, 16);
-            } else if constexpr (RPT * sizeof(I) == 8) {
-                int2 raw = __ldcs(reinterpret_cast<const int2 *>(col + base));
-                memcpy(cc, &raw, 8);
-            } else {
-#pragma unroll
-                for (int r = 0; r < RPT; ++r) cc[r] = __ldcs(col + base + r);
-            }
-#pragma unroll
-            for (int r = 0; r < RPT; ++r)
-                if (cc[r] >= 0) acc[r] = addd(acc[r], mulp(vv[r], __ldg(b + (int64_t)cc[r] * ldb)));
-        }
+        padded_rows<V, I, RPT>(val, col, b, ldb, i0, stride, width, acc);
 #pragma unroll
         for (int r = 0; r < RPT; ++r)
             if (i0 + r < rows) epi.row(i0 + r, acc[r], part);
@@ -546,31 +616,7 @@ __global__ void __launch_bounds__(256) sellp_kernel(int64_t rows, int64_t S,
         double acc[RPT];
 #pragma unroll
         for (int r = 0; r < RPT; ++r) acc[r] = 0.0;
-        for (int64_t k = 0; k < len; ++k) {
-            const int64_t base = off + k * S;
-            V vv[RPT];
-            I cc[RPT];
-            if constexpr (RPT * sizeof(V) == 16) {
-                int4 raw = __ldcs(reinterpret_cast<const int4 *>(val + base));
-                memcpy(vv, &raw, 16);
-            } else {
-#pragma unroll
-                for (int r = 0; r < RPT; ++r) vv[r] = __ldcs(val + base + r);
-            }
-            if constexpr (RPT * sizeof(I) == 16) {
-                int4 raw = __ldcs(reinterpret_cast<const int4 *>(col + base));
-                memcpy(cc, &raw, 16);
-            } else if constexpr (RPT * sizeof(I) == 8) {
-                int2 raw = __ldcs(reinterpret_cast<const int2 *>(col + base));
-                memcpy(cc, &raw, 8);
-            } else {
-#pragma unroll
-                for (int r = 0; r < RPT; ++r) cc[r] = __ldcs(col + base + r);
-            }
-#pragma unroll
-            for (int r = 0; r < RPT; ++r)
-                if (cc[r] >= 0) acc[r] = addd(acc[r], mulp(vv[r], __ldg(b + (int64_t)cc[r] * ldb)));
-        }
+        padded_rows<V, I, RPT>(val, col, b, ldb, off, S, len, acc);
 #pragma unroll
         for (int r = 0; r < RPT; ++r)
             if (i0 + r < rows) epi.row(i0 + r, acc[r], part);

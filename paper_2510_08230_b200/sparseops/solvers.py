@@ -22,8 +22,8 @@ import torch
 
 from .. import _lib
 from .core import DenseMatrix, dense_create
-from .errors import (DimensionMismatchError, InvalidArgumentError, PrecisionMismatchError,
-                     UnsupportedFeatureError)
+from .errors import (BreakdownError, DimensionMismatchError, InvalidArgumentError,
+                     NumericFailureError, PrecisionMismatchError, UnsupportedFeatureError)
 from .formats import _SparseBase, _stream
 from .linop import LinOp
 from .precond import JacobiPreconditioner
@@ -206,6 +206,11 @@ class _SolverBase(LinOp):
         bs, xs = bb.struct(), xx.struct()
         name = f"sb_{self._kind}_solve_{a._suffix()}"
         inv_p = ctypes.c_void_p(inv.data_ptr() if inv is not None else 0)
+        def _log():
+            hl = min(int(log.history_len), cap)
+            return ConvergenceLog(int(log.iterations), hist[:hl].tolist(), bool(log.converged),
+                                  STOP_RESIDUAL if log.stop_reason == 0 else STOP_MAX_ITERS)
+
         try:
             if self._kind == "gmres":
                 _lib.call(name, ctypes.byref(mat), inv_p, ctypes.byref(bs), ctypes.byref(xs),
@@ -215,12 +220,13 @@ class _SolverBase(LinOp):
                 _lib.call(name, ctypes.byref(mat), inv_p, ctypes.byref(bs), ctypes.byref(xs),
                           ctypes.byref(crit), ctypes.c_void_p(ws.data_ptr()), ctypes.byref(log),
                           _stream(a.device))
+        except (BreakdownError, NumericFailureError) as exc:
+            exc.log = _log()  # residual history up to the failure (diagnostics)
+            raise
         finally:
             if xx is not x:
                 x.array.copy_(xx.array)
-        hl = min(int(log.history_len), cap)
-        return ConvergenceLog(int(log.iterations), hist[:hl].tolist(), bool(log.converged),
-                              STOP_RESIDUAL if log.stop_reason == 0 else STOP_MAX_ITERS)
+        return _log()
 
 
 def _packed(v: DenseMatrix) -> bool:

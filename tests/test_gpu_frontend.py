@@ -1,0 +1,176 @@
+"""GPU tests of the drop-in frontend (the reference's pkg/frontend/tests, restated for the
+``cuda`` device): the Listing-1 / Listing-2 programs run verbatim with
+``pg.device("cuda")``, dispatch reaches every typed instantiation, zero-copy torch
+interop, and core error kinds cross the binding boundary unchanged."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2510_08230_b200.pysparseops as pg
+from paper_2510_08230_b200 import sparseops as core
+from paper_2510_08230_b200.pysparseops import bindings
+from tests.gpu_util import host
+
+pytestmark = pytest.mark.gpu
+
+# Listing 1 of the paper / test_pipeline_example.py:11-37, with the CUDA device and the
+# device Jacobi preconditioner (ILU is outside the B200 hot path)
+PIPELINE = """
+import paper_2510_08230_b200.pysparseops as pg
+import numpy as np
+
+fn = 'm1.mtx'
+dev = pg.device("cuda")
+mtx = pg.read(device=dev, path=fn, dtype="double", format="Csr")
+n_rows = mtx.size[0]
+
+b = pg.as_tensor(
+  device=dev, dim=(n_rows,1), dtype="double", fill=1.0
+)
+x = pg.as_tensor(
+  device=dev, dim=(n_rows,1), dtype="double", fill=0.0
+)
+
+# Create Jacobi preconditioner
+preconditioner = pg.preconditioner.Jacobi(dev, mtx)
+
+#Setup GMRES solver
+solver = pg.solver.gmres(dev, mtx, preconditioner,
+    max_iters=1000, krylov_dim=30, reduction_factor=1e-06
+)
+
+#Apply
+logger, result = solver.apply(b, x)
+"""
+
+
+@pytest.fixture
+def mtx_file(tmp_path, monkeypatch):
+    p = 6
+    n = p * p
+    trip = []
+    for gy in range(p):
+        for gx in range(p):
+            i = gy * p + gx
+            trip.append((i, i, 4.0))
+            for j in (i - 1 if gx else None, i + 1 if gx < p - 1 else None,
+                      i - p if gy else None, i + p if gy < p - 1 else None):
+                if j is not None:
+                    trip.append((i, j, -1.0))
+    dev = pg.device("cuda")
+    m = core.csr_from_coo(core.coo_from_triplets(dev, n, n, trip))
+    core.write_matrix_market(tmp_path / "m1.mtx", m)
+    monkeypatch.chdir(tmp_path)
+    return m
+
+
+def test_listing1_runs_verbatim(mtx_file):
+    ns = {}
+    exec(compile(PIPELINE, "pipeline_example", "exec"), ns)
+    logger, result, x, b, mtx = ns["logger"], ns["result"], ns["x"], ns["b"], ns["mtx"]
+    assert result is x
+    assert logger.converged and logger.stop_reason == "residual"
+    assert len(logger.residual_history) == logger.iterations >= 1
+    dense = mtx.to_dense()
+    bv, xv = host(b), host(result)
+    assert np.linalg.norm(bv - dense @ xv) / np.linalg.norm(bv) <= 1e-6 * (1 + 1e-8)
+    np.testing.assert_array_equal(bv, np.ones(mtx.rows))
+
+
+def test_listing2_config_solve(mtx_file):
+    dev = pg.device("cuda")
+    mtx = pg.read(dev, "m1.mtx")
+    args = {"type": "solver::Gmres", "krylov_dim": 30,
+            "preconditioner": {"type": "preconditioner::Jacobi"},
+            "criteria": [{"type": "Iteration", "max_iters": 1000},
+                         {"type": "ResidualNorm", "reduction_factor": 1e-06}]}
+    b = pg.as_tensor(device=dev, dim=(mtx.rows, 1), fill=1.0)
+    x = pg.as_tensor(device=dev, dim=(mtx.rows, 1), fill=0.0)
+    logger, result = pg.solve(args, mtx, b, x)
+    assert result is x and logger.converged
+
+
+def test_dispatch_reaches_every_instantiation():
+    """test_dispatch.py:19-50: each (value, index) combination routes to its binding."""
+    dev = pg.device("cuda")
+    rng = np.random.default_rng(3)
+    dense = (rng.random((9, 7)) < 0.3) * rng.standard_normal((9, 7))
+    for vname, vdt in bindings.VALUE_DTYPES.items():
+        for iname, idt in bindings.INDEX_DTYPES.items():
+            prec = core.Precision.from_dtype(vdt)
+            iw = core.IndexWidth.from_dtype(idt)
+            csr = core.csr_from_dense(dev, dense, prec, iw)
+            mats = {"csr": csr, "coo": core.coo_from_csr(csr), "ell": core.ell_from_csr(csr),
+                    "sellp": core.sellp_from_csr(csr), "hybrid": core.hybrid_from_csr(csr)}
+            b = pg.as_tensor(rng.standard_normal(7).astype(vdt), device=dev)
+            for fmt, m in mats.items():
+                x = pg.as_tensor(device=dev, dim=9, dtype=vname, fill=0.0)
+                pg.spmv(m, b, x)
+                np.testing.assert_allclose(host(x), dense.astype(vdt) @ host(b), rtol=1e-5,
+                                           atol=1e-5, err_msg=f"{fmt} {vname} {iname}")
+                fn = getattr(bindings, f"{fmt}_spmv_{vname}_{iname}")
+                fn(m, b, x)
+                with pytest.raises(pg.InstantiationMismatchError):
+                    other = "float" if vname == "double" else "double"
+                    getattr(bindings, f"{fmt}_spmv_{other}_{iname}")(m, b, x)
+    with pytest.raises(pg.NoMatchingInstantiationError):
+        pg.spmv(csr, pg.as_tensor(np.ones(7), device=dev), pg.as_tensor(device=dev, dim=9, dtype="float", fill=0.0))
+
+
+def test_zero_copy_torch_tensors():
+    """test_tensor.py:11-40 with CUDA tensors: shared memory both ways, copies flagged."""
+    dev = pg.device("cuda")
+    src = torch.tensor([1.0, 2.0, 3.0], device="cuda")
+    t = pg.as_tensor(src, device=dev)
+    assert t.copied is False
+    src[0] = 9.0
+    assert pg.dot(t, t) == 81.0 + 4.0 + 9.0
+    t.values[1] = -5.0
+    assert float(src[1]) == -5.0
+    f32 = torch.ones(4, dtype=torch.float32, device="cuda")
+    c = pg.as_tensor(f32, device=dev, dtype="double")
+    assert c.copied and c.values.dtype == torch.float64
+    with pytest.raises(pg.CopyRequiredError):
+        pg.as_tensor(f32, device=dev, dtype="double", copy=False)
+    h = pg.as_tensor(np.arange(4.0), device=dev)  # host data crosses to the device: a copy
+    assert h.copied and pg.norm2(h) == pytest.approx(np.sqrt(14.0))
+    with pytest.raises(pg.CopyRequiredError):
+        pg.as_tensor(np.arange(4.0), device=dev, copy=False)
+
+
+def test_error_kinds_cross_the_boundary():
+    """test_solve_api.py:146-152: core exception classes surface unchanged."""
+    dev = pg.device("cuda")
+    zero = core.csr_from_dense(dev, np.zeros((2, 2)))
+    b = pg.as_tensor(np.array([1.0, 2.0]), device=dev)
+    x = pg.as_tensor(device=dev, dim=2, fill=0.0)
+    with pytest.raises(core.errors.BreakdownError) as exc:
+        pg.solver.cg(dev, zero, None, max_iters=10).apply(b, x)
+    assert exc.value.kind == "breakdown" and exc.value.iteration == 1
+    with pytest.raises(core.errors.SingularDiagonalError) as exc:
+        pg.preconditioner.Jacobi(dev, zero)
+    assert exc.value.kind == "singular-diagonal" and exc.value.row == 0
+    a = core.csr_from_dense(dev, np.eye(3))
+    with pytest.raises(core.errors.DimensionMismatchError):
+        pg.spmv(a, pg.as_tensor(np.ones(2), device=dev), pg.as_tensor(device=dev, dim=3, fill=0.0))
+    with pytest.raises(core.errors.ConfigError) as exc:
+        pg.solve({"type": "solver::Cg", "criteria": []}, a, b, x)
+    assert exc.value.path == "criteria"
+
+
+def test_matrix_constructors():
+    import scipy.sparse as sps
+
+    dev = pg.device("cuda")
+    m = sps.random(40, 40, density=0.1, random_state=4, format="csr") + sps.eye(40) * 5
+    for fmt in ("csr", "coo", "ell", "sellp", "hybrid"):
+        a = pg.matrix(dev, m, format=fmt)
+        np.testing.assert_allclose(a.to_dense(), m.toarray(), rtol=0, atol=1e-15)
+    t = pg.matrix(dev, torch.tensor(m.toarray()).to_sparse())
+    np.testing.assert_array_equal(t.to_dense(), m.toarray())
+    logger, x = pg.solver.bicgstab(dev, pg.matrix(dev, m), max_iters=200,
+                                   reduction_factor=1e-10).apply(
+        pg.as_tensor(np.ones(40), device=dev), pg.as_tensor(device=dev, dim=40, fill=0.0))
+    assert logger.converged
+    np.testing.assert_allclose(m @ host(x), np.ones(40), atol=1e-8)
