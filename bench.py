@@ -191,9 +191,17 @@ def _spmv_roofline(a, dev, stream, torch, sp):
     spmv_bytes = a.precision.itemsize * (nnz + n + a.cols) + a.index_width.itemsize * (nnz + n + 1)
     peak, peak_kind = _peaks()
     achieved = spmv_bytes / (spmv_ms / 1e3) / 1e9
+    traffic = None
+    try:  # DRAM bytes per launch from the committed ncu --set full capture of this kernel
+        with open(os.path.join(REPO, "profiles", "r1_spmv_traffic.json")) as fh:
+            t = json.load(fh)
+        if t["algorithmic_bytes"] == spmv_bytes:
+            traffic = t["traffic"]
+    except Exception:
+        pass
     return spmv_ms, spmv_bytes, {
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-        "traffic": None, "kernel": f"csr_{a.kernel}_kernel<double,int>",
+        "traffic": traffic, "kernel": f"csr_{a.kernel}_kernel<double,int>",
         "alg_bytes_per_launch": spmv_bytes, "peak_source": peak_kind}
 
 
