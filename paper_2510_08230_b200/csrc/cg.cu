@@ -144,6 +144,8 @@ sb_status cg_solve(const SolveArgs &a) {
     spec.key = "cg" + std::to_string(sizeof(V)) + std::to_string(sizeof(I)) + "|" + matrix_key(M) +
                ptr_key({a.inv, b, x, a.ws});
     spec.poll_chunk = 8;
+    spec.hot_base = r;  // r, z, p, q, t are contiguous in the workspace
+    spec.hot_bytes = 5 * w.vec_bytes;
     spec.setup = [=](cudaStream_t st) -> cudaError_t {
         cudaError_t e = matrix_apply<V, I>(M, x, 1, t, 1, EpiStore<V>{t, 1}, st);
         if (e != cudaSuccess) return e;

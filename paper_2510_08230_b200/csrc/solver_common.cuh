@@ -290,6 +290,8 @@ struct LoopSpec {
     std::function<cudaError_t(cudaStream_t)> setup;    // enqueued once before the loop
     std::function<cudaError_t(cudaStream_t)> body;     // one loop iteration (or GMRES cycle)
     int poll_chunk;                                    // iterations per host poll (fallback)
+    void *hot_base = nullptr;                          // L2-persisting window (work vectors)
+    size_t hot_bytes = 0;
 };
 
 // Writes the initial control block (with the loop's conditional handle), enqueues

@@ -1,5 +1,6 @@
 // solver_runtime.cu -- the CUDA-graph WHILE loop runner shared by every solver, the
 // graph-cache keys, and the library-level solver entry points.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 
@@ -19,6 +20,33 @@ struct GraphEntry {
 
 static std::mutex g_cache_mu;
 static std::map<std::string, GraphEntry> g_cache;
+
+// Keep the Krylov work vectors resident in L2 while the matrix streams through it:
+// an access-policy window (hits persist, misses stream) on the capture stream, which
+// the captured kernel nodes inherit.  Size of the persisting carve-out from
+// SPARSEB200_L2_PERSIST_MB (0 disables).
+static void apply_l2_window(cudaStream_t cs, void *base, size_t bytes) {
+    static const long mb = [] {
+        const char *e = getenv("SPARSEB200_L2_PERSIST_MB");
+        return e ? atol(e) : 0L;
+    }();
+    if (mb <= 0 || !base || !bytes) return;
+    int dev = 0, max_persist = 0, max_window = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    size_t carve = std::min<size_t>((size_t)mb << 20, (size_t)max_persist);
+    if (carve == 0 || max_window <= 0) return;
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve);
+    cudaStreamAttrValue v = {};
+    v.accessPolicyWindow.base_ptr = base;
+    v.accessPolicyWindow.num_bytes = std::min<size_t>(bytes, (size_t)max_window);
+    v.accessPolicyWindow.hitRatio = std::min(1.0f, (float)carve / (float)v.accessPolicyWindow.num_bytes);
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cudaStreamSetAttribute(cs, cudaStreamAttributeAccessPolicyWindow, &v);
+    cudaGetLastError();
+}
 
 static cudaError_t build_while_graph(const LoopSpec &spec, GraphEntry &out) {
     cudaGraph_t g = nullptr;
@@ -48,6 +76,7 @@ static cudaError_t build_while_graph(const LoopSpec &spec, GraphEntry &out) {
         cudaGraphDestroy(g);
         return e;
     }
+    apply_l2_window(cs, spec.hot_base, spec.hot_bytes);
     e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
     if (e == cudaSuccess) {
         cudaError_t eb = spec.body(cs);

@@ -36,3 +36,8 @@ torch.cuda.synchronize()
 ms = e0.elapsed_time(e1)
 print(f"fused={os.environ.get('SPARSEB200_CG_FUSED', '1')} R={R} p={p} iters={log.iterations} "
       f"solve={ms / 5:.3f} ms  per-iter={ms / its * 1e3:.2f} us")
+try:
+    import ctypes
+    print("  L2 persist attr:", torch.cuda.get_device_properties(0).L2_cache_size // (1 << 20), "MB L2")
+except Exception:
+    pass
