@@ -226,7 +226,7 @@ sb_status sb_csr_plan_select(const sb_row_stats *stats, int32_t value_bytes, int
     SB_GUARD_END
 }
 
-int64_t sb_coo_tile_entries(void) { return kCooNT * kCooIPT; }
+int64_t sb_coo_tile_entries(void) { return kCooChunk; }
 
 #define SB_IDX_SPMV_DEFS(I, IN)                                                                    \
     sb_status sb_csr_row_stats_##IN(int64_t rows, const void *row_ptrs, void *workspace,           \

@@ -512,6 +512,104 @@ __global__ void __launch_bounds__(NT) coo_kernel(int64_t rows, int64_t nnz, cons
     }
 }
 
+// ============================================================ COO: warp segmented reduction
+// Every warp owns chunks of CHUNK consecutive (sorted) entries.  Per step each lane
+// loads K entries (entry base + k*32 + lane: coalesced), issues the K gathers, then for
+// each k the warp runs an inclusive shuffle scan by row key (5 steps, fixed order); a
+// lane whose successor holds another key closes its run and writes it, the open run at
+// lane 31 is carried in registers to the next group.  The run still open at the end of a
+// chunk is written by the chunk that finishes the row, its partial goes to the carry
+// fix-up (deterministic, no atomics).  Empty rows between keys are zeroed by the lane
+// that sees the gap (accumulate == false).  No shared memory, no block barriers.
+template <class V, class I, int K>
+__global__ void __launch_bounds__(256) coo_warp_kernel(int64_t rows, int64_t nnz,
+                                                       const I *__restrict__ ri,
+                                                       const I *__restrict__ ci,
+                                                       const V *__restrict__ val,
+                                                       const V *__restrict__ b, int64_t ldb, V *x,
+                                                       int64_t ldx, int64_t chunk, int64_t nchunks,
+                                                       int64_t *carry_rows, double *carry_vals,
+                                                       bool accumulate) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    constexpr int64_t NONE = INT64_MAX;
+    for (int64_t c = warp; c < nchunks; c += nwarps) {
+        const int64_t e0 = c * chunk;
+        const int64_t e1 = e0 + chunk < nnz ? e0 + chunk : nnz;
+        int64_t ckey = e0 == 0 ? -1 : (int64_t)ri[e0 - 1];  // key before the first entry
+        double cval = 0.0;
+        bool open = false;  // (ckey, cval) is a run opened inside this chunk
+        for (int64_t base = e0; base < e1; base += 32 * K) {
+            int64_t key[K];
+            V vv[K], gg[K];
+            I cc[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int64_t e = base + k * 32 + lane;
+                if (e < e1) {
+                    key[k] = (int64_t)ld_stream(ri + e);
+                    cc[k] = ld_stream(ci + e);
+                    vv[k] = ld_stream(val + e);
+                } else {
+                    key[k] = NONE;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+                if (key[k] != NONE) gg[k] = __ldg(b + (int64_t)cc[k] * ldb);
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int64_t kk = key[k];
+                double v = kk != NONE ? mulp(vv[k], gg[k]) : 0.0;
+                if (!accumulate) {  // zero the empty rows between the previous key and this one
+                    int64_t prev = __shfl_up_sync(0xffffffffu, kk, 1);
+                    if (lane == 0) prev = ckey;
+                    if (kk != NONE)
+                        for (int64_t g = prev + 1; g < kk; ++g) x[g * ldx] = (V)0;
+                }
+                // the run carried from the previous group ends where this group starts a new row
+                const int64_t k0 = __shfl_sync(0xffffffffu, kk, 0);
+                if (open && k0 != ckey) {
+                    if (lane == 0) x[ckey * ldx] = accumulate ? (V)addd((double)x[ckey * ldx], cval) : (V)cval;
+                    open = false;
+                }
+                if (lane == 0 && open && kk == ckey) v = addd(cval, v);
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int64_t k2 = __shfl_up_sync(0xffffffffu, kk, o);
+                    const double v2 = __shfl_up_sync(0xffffffffu, v, o);
+                    if (lane >= o && k2 == kk) v = addd(v2, v);
+                }
+                const int64_t next = __shfl_down_sync(0xffffffffu, kk, 1);
+                if (lane < 31 && kk != NONE && next != kk)
+                    x[kk * ldx] = accumulate ? (V)addd((double)x[kk * ldx], v) : (V)v;
+                const int64_t k31 = __shfl_sync(0xffffffffu, kk, 31);
+                const double v31 = __shfl_sync(0xffffffffu, v, 31);
+                if (k31 != NONE) {  // lane 31's run stays open into the next group
+                    ckey = k31;
+                    cval = v31;
+                    open = true;
+                } else {  // past the chunk end: every run closed at its last valid lane
+                    open = false;
+                }
+            }
+        }
+        // the run open at the end of the chunk: finished here, or carried to the next chunk
+        if (lane == 0) {
+            const int64_t after = e1 < nnz ? (int64_t)ri[e1] : NONE;
+            const bool carry = open && after == ckey;
+            if (open && !carry) x[ckey * ldx] = accumulate ? (V)addd((double)x[ckey * ldx], cval) : (V)cval;
+            carry_rows[c] = carry ? ckey : -1;
+            carry_vals[c] = carry ? cval : 0.0;
+            if (!accumulate && c == nchunks - 1 && e1 == nnz) {
+                const int64_t last = (int64_t)ri[nnz - 1];
+                for (int64_t g = last + 1; g < rows; ++g) x[g * ldx] = (V)0;
+            }
+        }
+    }
+}
+
 // ============================================================ padded layouts (ELL / SELL-P)
 // One column of RPT consecutive rows: 16-byte value vector and 8/16-byte index vector.
 template <class V, class I, int RPT>

@@ -169,21 +169,27 @@ cudaError_t csr_apply(const sb_csr &A, const V *b, int64_t ldb, V *x_out, int64_
 }
 
 // ---------------------------------------------------------------- COO
+constexpr int kCooK = 4;                      // entries per lane per warp step
+constexpr int64_t kCooChunk = 32 * kCooK * 8;  // entries per warp chunk (carry granularity)
+
 template <class V, class I>
 cudaError_t coo_raw(const sb_coo &A, const V *b, int64_t ldb, V *x, int64_t ldx, bool accumulate,
                     cudaStream_t st) {
     if (A.rows == 0) return cudaSuccess;
     if (A.nnz == 0) return accumulate ? cudaSuccess : launch_fill<V>(A.rows, 1, x, ldx, (V)0, st);
     const sb_coo_plan &P = *A.plan;
-    auto kern = coo_kernel<V, I, kCooNT, kCooIPT>;
-    int grid = persistent_grid(kern, kCooNT, 0);
-    if (grid > P.num_tiles) grid = (int)P.num_tiles;
-    kern<<<grid, kCooNT, 0, st>>>(A.rows, A.nnz, (const I *)A.row_idxs, (const I *)A.col_idxs,
-                                  (const V *)A.values, b, ldb, x, ldx, P.num_tiles,
-                                  (int64_t *)P.carry_rows, (double *)P.carry_vals, accumulate);
+    const int64_t nchunks = ceil_div(A.nnz, kCooChunk);
+    if (nchunks > P.num_tiles) return cudaErrorInvalidValue;  // carry buffers too small
+    auto kern = coo_warp_kernel<V, I, kCooK>;
+    int grid = persistent_grid(kern, 256, 0);
+    const int64_t need = ceil_div(nchunks * 32, 256);
+    if (grid > need) grid = (int)need;
+    kern<<<grid, 256, 0, st>>>(A.rows, A.nnz, (const I *)A.row_idxs, (const I *)A.col_idxs,
+                               (const V *)A.values, b, ldb, x, ldx, kCooChunk, nchunks,
+                               (int64_t *)P.carry_rows, (double *)P.carry_vals, accumulate);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    return launch_fixup<V>(P.num_tiles, (const int64_t *)P.carry_rows, (const double *)P.carry_vals,
+    return launch_fixup<V>(nchunks, (const int64_t *)P.carry_rows, (const double *)P.carry_vals,
                            x, ldx, st);
 }
 

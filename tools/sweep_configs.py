@@ -28,12 +28,23 @@ PEAK = 6543.1
 
 
 def timed_spmv(mat, b, x, reps=20, flush=None):
+    """Average launch time.  Without a flush: `reps` back-to-back launches between two
+    events (the matrix is larger than L2).  With a flush: a 256 MB read before every
+    launch, whose runtime hides the host enqueue latency of the timed launch."""
     for _ in range(3):
         mat.apply(b, x)
+    torch.cuda.synchronize()
+    if flush is None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            mat.apply(b, x)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps * 1e3  # us
     total = 0.0
     for _ in range(reps):
-        if flush is not None:
-            flush.sum()  # read-only sweep: L2 refilled with clean lines
+        flush.sum()  # read-only sweep: L2 refilled with clean lines
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         mat.apply(b, x)
@@ -69,23 +80,15 @@ def cpu_spmv(rp, ci, v, b, threads, reps=5):
     return float(np.median(ts))
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--skip-cpu", action="store_true")
-    args = ap.parse_args()
-    dev = sp.create_device("cuda", 0)
-    threads = len(os.sched_getaffinity(0))
-    out = {"host_threads": threads}
-    flush = torch.zeros(32 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 256 MB
-
-    # ---------------- #1
+def config1(dev, out, args, threads, flush):
     a = gen.poisson2d(dev, 1000)
     b = sp.dense_from_array(dev, torch.tensor(np.random.default_rng(0).random(a.rows)))
     x = sp.dense_create(dev, a.rows, 1, sp.Precision.double, 0.0)
     us = timed_spmv(a, b, x, flush=flush)
     byt = fmt_bytes(a, 8, 4)
     rec = {"kernel": a.kernel, "us": us, "gbs": byt / us / 1e3, "frac": byt / us / 1e3 / PEAK,
-           "gflops": 2 * a.nnz / us / 1e3, "bytes": byt, "l2": "flushed (256 MB read) before every launch"}
+           "gflops": 2 * a.nnz / us / 1e3, "bytes": byt,
+           "l2": "flushed (256 MB read) before every launch"}
     if not args.skip_cpu:
         rp, ci, v = (t.cpu().numpy() for t in (a.row_ptrs, a.col_idxs, a.values))
         bv = b.numpy()[:, 0]
@@ -93,9 +96,30 @@ def main():
         rec[f"cpu_{threads}threads_s"] = cpu_spmv(rp, ci, v, bv, threads)
     out["config1_poisson2d_1000_csr_f64"] = rec
     print(json.dumps({"config1": rec}), file=sys.stderr)
-    del a
 
-    # ---------------- #3
+
+def config2(dev, out, args, threads, flush):
+    """Poisson 128^3 format sweep (north_star: CSR and SELL-P >= 75% of the roofline)."""
+    fsweep = {}
+    for vdt, prec in ((np.float64, sp.Precision.double), (np.float32, sp.Precision.single)):
+        a = gen.poisson3d(dev, 128, precision=prec)
+        vb = prec.itemsize
+        b = sp.dense_create(dev, a.rows, 1, prec, 1.0)
+        x = sp.dense_create(dev, a.rows, 1, prec, 0.0)
+        res = {}
+        for name, m in {"csr": a, "coo": sp.coo_from_csr(a), "ell": sp.ell_from_csr(a),
+                        "sellp64": sp.sellp_from_csr(a, 64), "sellp32": sp.sellp_from_csr(a, 32),
+                        "hybrid": sp.hybrid_from_csr(a)}.items():
+            us = timed_spmv(m, b, x)
+            byt = fmt_bytes(m, vb, 4)
+            res[name] = {"us": us, "format_bytes": byt, "gbs": byt / us / 1e3,
+                         "frac": byt / us / 1e3 / PEAK}
+        fsweep[np.dtype(vdt).name] = res
+        print(json.dumps({"config2_formats": np.dtype(vdt).name, "res": res}), file=sys.stderr)
+    out["config2_poisson128_formats"] = fsweep
+
+
+def config3(dev, out, args, threads, flush):
     sweep = {}
     for vdt, prec in ((np.float64, sp.Precision.double), (np.float32, sp.Precision.single)):
         a = gen.powerlaw_csr(dev, precision=prec)
@@ -129,7 +153,8 @@ def main():
         torch.cuda.empty_cache()
     out["config3_powerlaw_4M"] = sweep
 
-    # ---------------- #4
+
+def config4(dev, out, args, threads, flush):
     a = gen.convdiff3d(dev, 256)
     m = sp.jacobi_create(a)
     solves = {}
@@ -137,19 +162,38 @@ def main():
         s = cls(a, criteria=[sp.Iteration(5000), sp.ResidualNorm(1e-8)], preconditioner=m, **kw)
         b = sp.dense_create(dev, a.rows, 1, sp.Precision.double, 1.0)
         x = sp.dense_create(dev, a.rows, 1, sp.Precision.double, 0.0)
-        s.solve(b, x)  # warm (graph capture)
-        x.values.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        log = s.solve(b, x)
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
-        solves[name] = {"iterations": log.iterations, "converged": log.converged,
-                        "final_residual": log.residual_history[-1], "solve_ms": ms,
-                        "ms_per_iteration": ms / max(log.iterations, 1)}
+        try:
+            s.solve(b, x)  # warm (graph capture)
+            x.values.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            log = s.solve(b, x)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            solves[name] = {"iterations": log.iterations, "converged": log.converged,
+                            "final_residual": log.residual_history[-1], "solve_ms": ms,
+                            "ms_per_iteration": ms / max(log.iterations, 1)}
+        except (sp.errors.BreakdownError, sp.errors.NumericFailureError) as exc:
+            h = exc.log.residual_history
+            solves[name] = {"error": f"{exc.kind} at iteration {getattr(exc, 'iteration', '?')}",
+                            "max_residual": max(h) if h else None}
         print(json.dumps({"config4": name, "res": solves[name]}), file=sys.stderr)
     out["config4_convdiff256_f64"] = solves
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--only", default="1,2,3,4", help="comma list of configs to run")
+    args = ap.parse_args()
+    dev = sp.create_device("cuda", 0)
+    threads = len(os.sched_getaffinity(0))
+    out = {"host_threads": threads}
+    flush = torch.zeros(32 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 256 MB
+    for c in args.only.split(","):
+        {"1": config1, "2": config2, "3": config3, "4": config4}[c.strip()](dev, out, args, threads, flush)
+        torch.cuda.empty_cache()
     print(json.dumps(out))
 
 
