@@ -131,10 +131,13 @@ typedef struct {
     const void *col_idxs, *values;
 } sb_ell;
 
-/* SELL-P(slice_size): entry k of row i (slice s = i / S) at (slice_sets[s] + k)*S + i%S */
+/* SELL-P(slice_size): entry k of row i (slice s = i / S) at (slice_sets[s] + k)*S + i%S.
+ * max_block_entries: max stored entries of any 128/S consecutive slices (aligned), for the
+ * TMA-staged kernel (0 = use the direct kernel). */
 typedef struct {
     int64_t rows, cols, slice_size, num_slices;
     const void *slice_lengths, *slice_sets, *col_idxs, *values;
+    int64_t max_block_entries;
 } sb_sellp;
 
 /* Hybrid(w): the first min(len_i, w) entries of each row in ELL(w), the rest in COO */

@@ -722,6 +722,128 @@ __global__ void __launch_bounds__(256) sellp_kernel(int64_t rows, int64_t S,
     epi.finish(part);
 }
 
+// ============================================================ SELL-P: TMA-staged slices
+// A block of SPB = 128 / S consecutive slices is one contiguous range of the value and
+// column arrays ((slice_sets[s0] .. slice_sets[s0 + SPB]) * S entries), so it is staged
+// exactly like a CSR stream block: one elected thread issues cp.async.bulk copies into a
+// two-stage shared-memory ring (mbarrier completion), the next block is prefetched
+// while this one is reduced, and thread t reduces row t of the block sequentially
+// (column-major within the slice) -> bit-exact with the reference's row order.
+struct SellpMeta {
+    int64_t s0;              // first slice of the block
+    int64_t dv, dc;          // stage slot of the block's first entry (values / columns)
+    int32_t len[4], off[4];  // per slice: length, first entry relative to the block start
+};
+
+template <class V, class I, int S, class Epi>
+__global__ void __launch_bounds__(128) sellp_stream_kernel(int64_t rows, int64_t nslices,
+                                                           const I *__restrict__ sl,
+                                                           const I *__restrict__ ss,
+                                                           const I *__restrict__ col,
+                                                           const V *__restrict__ val,
+                                                           const V *__restrict__ b, int64_t ldb,
+                                                           int cap_entries, Epi epi) {
+    constexpr int SPB = 128 / S;
+    static_assert(SPB >= 1 && SPB <= 4, "slice size 32, 64 or 128");
+    if (epi.skip()) return;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ SellpMeta meta[2];
+    constexpr int VV = 16 / sizeof(V), VI = 16 / sizeof(I);
+    const size_t cap_v = (size_t)cap_entries + 2 * VV, cap_c = (size_t)cap_entries + 2 * VI;
+    const size_t off_c = (cap_v * sizeof(V) + 15) & ~size_t(15);
+    const size_t stage_bytes = (off_c + cap_c * sizeof(I) + 15) & ~size_t(15);
+    const int tid = threadIdx.x;
+    const int64_t nblk = (nslices + SPB - 1) / SPB;
+    const int64_t total = (int64_t)ss[nslices] * S;
+    const uint64_t pol = policy_evict_first();
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    auto issue = [&](int64_t blk, int st) {  // thread 0 only
+        unsigned char *p = smem + st * stage_bytes;
+        V *sv = reinterpret_cast<V *>(p);
+        I *sc = reinterpret_cast<I *>(p + off_c);
+        const int64_t s0 = blk * SPB, s1 = s0 + SPB < nslices ? s0 + SPB : nslices;
+        const int64_t lo = (int64_t)ss[s0] * S, hi = (int64_t)ss[s1] * S;
+        SellpMeta m;
+        m.s0 = s0;
+        int64_t bv_base = 0, bc_base = 0;
+        const uint32_t bv = stage_range(val, lo, hi, total, sv, bv_base);
+        const uint32_t bc = stage_range(col, lo, hi, total, sc, bc_base);
+        m.dv = lo - bv_base;
+        m.dc = lo - bc_base;
+        for (int j = 0; j < SPB; ++j) {
+            const int64_t s = s0 + j;
+            m.len[j] = s < s1 ? (int32_t)sl[s] : 0;
+            m.off[j] = s < s1 ? (int32_t)((int64_t)ss[s] * S - lo) : 0;
+        }
+        meta[st] = m;
+        mbar_arrive_expect_tx(&bar[st], bv + bc);
+        if (bv) bulk_g2s(sv, val + bv_base, bv, &bar[st], pol);
+        if (bc) bulk_g2s(sc, col + bc_base, bc, &bar[st], pol);
+    };
+    double part[Epi::N] = {};
+    int64_t blk = blockIdx.x;
+    if (tid == 0 && blk < nblk) issue(blk, 0);
+    for (int it = 0; blk < nblk; blk += gridDim.x, ++it) {
+        const int st = it & 1;
+        const uint32_t parity = (it >> 1) & 1;
+        if (tid == 0 && blk + gridDim.x < nblk) issue(blk + gridDim.x, st ^ 1);
+        mbar_wait(&bar[st], parity);
+        const unsigned char *p = smem + st * stage_bytes;
+        const V *sv = reinterpret_cast<const V *>(p);
+        const I *sc = reinterpret_cast<const I *>(p + off_c);
+        const SellpMeta m = meta[st];
+        const int j = tid / S, l = tid % S;
+        const int64_t i = (m.s0 + j) * S + l;
+        if (j < SPB && i < rows) {
+            const int64_t dv = m.dv, dc = m.dc;
+            const int len = m.len[j];
+            const int64_t o = m.off[j] + l;
+            double acc = 0.0;
+            int k = 0;
+            for (; k + 8 <= len; k += 8) {
+                V vv[8], bb[8];
+                I cc[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int64_t e = o + (int64_t)(k + u) * S;
+                    vv[u] = sv[dv + e];
+                    cc[u] = sc[dc + e];
+                    bb[u] = cc[u] >= 0 ? __ldg(b + (int64_t)cc[u] * ldb) : (V)0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (cc[u] >= 0) acc = addd(acc, mulp(vv[u], bb[u]));
+            }
+            if (k < len) {
+                V vv[8], bb[8];
+                I cc[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    cc[u] = (I)-1;
+                    if (k + u < len) {
+                        const int64_t e = o + (int64_t)(k + u) * S;
+                        vv[u] = sv[dv + e];
+                        cc[u] = sc[dc + e];
+                        if (cc[u] >= 0) bb[u] = __ldg(b + (int64_t)cc[u] * ldb);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (cc[u] >= 0) acc = addd(acc, mulp(vv[u], bb[u]));
+            }
+            epi.row(i, acc, part);
+        }
+        __syncthreads();
+    }
+    epi.finish(part);
+}
+
 // Row-owned epilogue applied after a row-splitting SpMV (merge / COO / Hybrid):
 // re-reads x and feeds it to the epilogue (so fused dots work for every format).
 template <class V, class Epi>

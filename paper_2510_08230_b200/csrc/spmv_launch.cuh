@@ -231,9 +231,41 @@ cudaError_t ell_apply(const sb_ell &A, const V *b, int64_t ldb, const Epi &epi, 
     return cudaGetLastError();
 }
 
+template <class V, class I, int S, class Epi>
+cudaError_t launch_sellp_stream(const sb_sellp &A, const V *b, int64_t ldb, const Epi &epi,
+                                cudaStream_t st) {
+    constexpr int VV = 16 / sizeof(V), VI = 16 / sizeof(I);
+    const int cap = (int)A.max_block_entries;
+    const size_t cap_v = (size_t)cap + 2 * VV, cap_c = (size_t)cap + 2 * VI;
+    const size_t off_c = (cap_v * sizeof(V) + 15) & ~size_t(15);
+    const size_t stage = (off_c + cap_c * sizeof(I) + 15) & ~size_t(15);
+    auto kern = sellp_stream_kernel<V, I, S, Epi>;
+    static int configured = 0;
+    if (!configured) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        configured = 1;
+    }
+    int grid = persistent_grid(kern, 128, 2 * stage);
+    const int64_t nblk = ceil_div(A.num_slices, 128 / S);
+    if (grid > nblk) grid = (int)nblk;
+    kern<<<grid, 128, 2 * stage, st>>>(A.rows, A.num_slices, (const I *)A.slice_lengths,
+                                       (const I *)A.slice_sets, (const I *)A.col_idxs,
+                                       (const V *)A.values, b, ldb, cap, epi);
+    return cudaGetLastError();
+}
+
 template <class V, class I, class Epi>
 cudaError_t sellp_apply(const sb_sellp &A, const V *b, int64_t ldb, const Epi &epi, cudaStream_t st) {
     if (A.rows == 0) return cudaSuccess;
+    const bool staged = A.max_block_entries > 0 &&
+                        2 * (size_t)A.max_block_entries * (sizeof(V) + sizeof(I)) <= 96 * 1024 &&
+                        ((uintptr_t)A.values % 16 == 0) && ((uintptr_t)A.col_idxs % 16 == 0) &&
+                        (A.slice_size == 32 || A.slice_size == 64 || A.slice_size == 128);
+    if (staged) {
+        if (A.slice_size == 64) return launch_sellp_stream<V, I, 64>(A, b, ldb, epi, st);
+        if (A.slice_size == 32) return launch_sellp_stream<V, I, 32>(A, b, ldb, epi, st);
+        return launch_sellp_stream<V, I, 128>(A, b, ldb, epi, st);
+    }
     constexpr int RPT = rows_per_thread<V, I>();
     const bool vec_ok = (A.slice_size % RPT == 0) && ((uintptr_t)A.values % 16 == 0) &&
                         ((uintptr_t)A.col_idxs % (RPT * sizeof(I) >= 16 ? 16 : RPT * sizeof(I)) == 0);

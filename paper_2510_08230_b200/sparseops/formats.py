@@ -331,11 +331,33 @@ class SellpMatrix(_SparseBase):
                 self.slice_sets.numel() != self.num_slices + 1:
             raise InvalidArgumentError("slice arrays do not match rows / slice_size")
         self._nnz = int((self.col_idxs >= 0).sum()) if nnz is None else int(nnz)
+        self.max_block_entries = self._block_entries()
+        self.staged = True  # TMA-staged slice kernel when the block fits shared memory
+
+    def with_staging(self, staged: bool) -> "SellpMatrix":
+        """Same arrays (shared), staged (TMA) or direct SpMV kernel."""
+        m = SellpMatrix(self.device, self.rows, self.cols, self.slice_size, self.slice_lengths,
+                        self.slice_sets, self.col_idxs, self.values, nnz=self._nnz)
+        m.staged = staged
+        return m
+
+    def _block_entries(self) -> int:
+        """Max stored entries of any aligned group of 128 / S slices (one TMA-staged block
+        of the sellp_stream kernel); 0 when the slice size has no staged kernel."""
+        S = self.slice_size
+        if S not in (32, 64, 128) or self.num_slices == 0:
+            return 0
+        spb = 128 // S
+        ss = self.slice_sets.long()
+        idx = torch.arange(0, self.num_slices, spb, device=ss.device)
+        hi = torch.clamp(idx + spb, max=self.num_slices)
+        return int(((ss[hi] - ss[idx]) * S).max())
 
     def struct(self) -> _lib.SbSellp:
         return _lib.SbSellp(self.rows, self.cols, self.slice_size, self.num_slices,
                             _ptr(self.slice_lengths).value, _ptr(self.slice_sets).value,
-                            _ptr(self.col_idxs).value, _ptr(self.values).value)
+                            _ptr(self.col_idxs).value, _ptr(self.values).value,
+                            self.max_block_entries if self.staged else 0)
 
     @property
     def stored(self) -> int:

@@ -49,7 +49,7 @@ def test_coo_ell_sellp_hybrid_on_golden_suite(dev, vdt, idt):
         rows, cols = (int(t) for t in m["shape"])
         a = csr(dev, m["row_ptrs"], m["col_idxs"], m["values"], cols)
         b = vec(dev, m["b"])
-        for fmt in ("coo", "ell", "sellp", "sellp32", "hybrid", "hybrid2"):
+        for fmt in ("coo", "ell", "sellp", "sellp32", "sellp_direct", "hybrid", "hybrid2"):
             if fmt == "coo":
                 mat = sp.coo_from_csr(a)
             elif fmt == "ell":
@@ -58,6 +58,8 @@ def test_coo_ell_sellp_hybrid_on_golden_suite(dev, vdt, idt):
                 mat = sp.sellp_from_csr(a, 64)
             elif fmt == "sellp32":
                 mat = sp.sellp_from_csr(a, 32)
+            elif fmt == "sellp_direct":
+                mat = sp.sellp_from_csr(a, 64).with_staging(False)
             elif fmt == "hybrid":
                 mat = sp.hybrid_from_csr(a)
             else:
@@ -65,7 +67,7 @@ def test_coo_ell_sellp_hybrid_on_golden_suite(dev, vdt, idt):
             x = out(dev, rows, m["values"].dtype)
             mat.apply(b, x)
             got = host(x)
-            if fmt in ("ell", "sellp", "sellp32"):
+            if fmt in ("ell", "sellp", "sellp32", "sellp_direct"):
                 np.testing.assert_array_equal(got, m["x"], err_msg=f"{fmt} {rows}x{cols}")
             elif fmt == "coo":
                 assert_close(got, m["x"], m["row_ptrs"], m["values"], m["b"])
@@ -192,7 +194,8 @@ def test_baseline_poisson_bitwise(dev, p, dim):
     x = out(dev, a.rows, np.float64)
     a.apply(vec(dev, bv), x)
     np.testing.assert_array_equal(host(x), sbref.csr_spmv(frp, fci, fv, bv, threads=8))
-    for conv in (sp.ell_from_csr, sp.sellp_from_csr):
+    for conv in (sp.ell_from_csr, sp.sellp_from_csr,
+                 lambda m: sp.sellp_from_csr(m).with_staging(False), lambda m: sp.sellp_from_csr(m, 32)):
         y = out(dev, a.rows, np.float64)
         conv(a).apply(vec(dev, bv), y)
         np.testing.assert_array_equal(host(y), host(x))
