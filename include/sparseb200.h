@@ -183,6 +183,10 @@ int sb_version(void);
 const char *sb_status_string(int code);
 /* CUDA graph + conditional-node solver loop (1, default) or host-polled launches (0) */
 void sb_set_graph_mode(int enabled);
+/* CG loop shape: 1 (default) = two kernels per iteration, the search direction evaluated
+   inside the SpMV gather (row-owning formats); 0 = three kernels (SpMV+dot, update,
+   direction).  Both produce bitwise identical iterates. */
+void sb_set_cg_fused(int enabled);
 
 #define SB_VALUE_DECLS(VN)                                                                       \
     /* core.dot / norm2 / axpy / scal / copy_into (core.py:358-401); jacobi apply (precond.py:57-63) */ \

@@ -182,7 +182,7 @@ sb_status bicgstab_solve(const SolveArgs &a) {
     Ctl h = initial_ctl(*a.crit, w, cap);
     LoopSpec spec;
     spec.key = "bicgstab" + std::to_string(sizeof(V)) + std::to_string(sizeof(I)) + "|" +
-               matrix_key(M) + ptr_key({a.inv, b, x, a.ws});
+               matrix_key(M) + ptr_key({a.inv, b, x, a.ws, w.vecs, w.hist, w.small});
     spec.poll_chunk = 8;
     spec.setup = [=](cudaStream_t st) -> cudaError_t {
         cudaError_t e = matrix_apply<V, I>(M, x, 1, t, 1, EpiStore<V>{t, 1}, st);

@@ -138,15 +138,6 @@ struct CgsResidualPass : SkipNone {
     }
 };
 
-inline bool row_owned_format(const sb_matrix &M) {
-    if (M.format == SB_FMT_ELL || M.format == SB_FMT_SELLP) return true;
-    if (M.format == SB_FMT_CSR) {
-        const sb_csr &A = *(const sb_csr *)M.mat;
-        return !A.plan || A.plan->kernel != SB_CSR_MERGE;
-    }
-    return false;
-}
-
 template <class V, class I>
 sb_status cgs_solve(const SolveArgs &a) {
     sb_error *err = a.err;
@@ -163,11 +154,11 @@ sb_status cgs_solve(const SolveArgs &a) {
     Ctl *ctl = w.ctl;
     double *part = w.partials;
     const sb_matrix M = *a.A;
-    const bool fused = row_owned_format(M);
+    const bool fused = matrix_row_owning(M);
     Ctl h = initial_ctl(*a.crit, w, cap);
     LoopSpec spec;
     spec.key = "cgs" + std::to_string(sizeof(V)) + std::to_string(sizeof(I)) + "|" + matrix_key(M) +
-               ptr_key({a.inv, b, x, a.ws});
+               ptr_key({a.inv, b, x, a.ws, w.vecs, w.hist, w.small});
     spec.poll_chunk = 8;
     spec.setup = [=](cudaStream_t st) -> cudaError_t {
         cudaError_t e = matrix_apply<V, I>(M, x, 1, t, 1, EpiStore<V>{t, 1}, st);

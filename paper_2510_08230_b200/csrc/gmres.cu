@@ -298,7 +298,7 @@ sb_status gmres_solve(const SolveArgs &a) {
     h.R = sm + 4 * (m + 2) + m;
     LoopSpec spec;
     spec.key = "gmres" + std::to_string(sizeof(V)) + std::to_string(sizeof(I)) + "|" + std::to_string(m) +
-               "|" + matrix_key(M) + ptr_key({a.inv, b, x, a.ws});
+               "|" + matrix_key(M) + ptr_key({a.inv, b, x, a.ws, w.vecs, w.hist, w.small});
     spec.poll_chunk = 1;
     spec.setup = [=](cudaStream_t st) -> cudaError_t {
         return launch_ew<1>(n, ctl, part, NormB<V>{{}, b}, st);

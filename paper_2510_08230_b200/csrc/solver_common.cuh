@@ -56,7 +56,9 @@ struct Ctl {
     double hnorm, beta_restart;
     int64_t cycle;
     double dot[8];  // row-partitioned solves: local dot totals, reduced across ranks in place
+    int32_t xpend;  // fused CG: x += alpha p of the last completed iteration still pending
 };
+static_assert(sizeof(Ctl) <= 4096, "control block must fit kCtlBytes");
 
 __device__ __forceinline__ void stop_loop(Ctl *c) {
     c->done = 1;
@@ -289,6 +291,7 @@ struct LoopSpec {
     std::string key;                                   // identifies the captured body
     std::function<cudaError_t(cudaStream_t)> setup;    // enqueued once before the loop
     std::function<cudaError_t(cudaStream_t)> body;     // one loop iteration (or GMRES cycle)
+    std::function<cudaError_t(cudaStream_t)> finish;   // enqueued once after the loop (optional)
     int poll_chunk;                                    // iterations per host poll (fallback)
     void *hot_base = nullptr;                          // L2-persisting window (work vectors)
     size_t hot_bytes = 0;

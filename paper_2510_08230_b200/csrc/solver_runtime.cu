@@ -155,6 +155,7 @@ sb_status run_loop(const LoopSpec &spec, Ctl *dctl, Ctl &hctl, cudaStream_t st, 
             }
         }
     }
+    if (spec.finish) SB_CUDA(spec.finish(st));
     SB_CUDA(cudaMemcpyAsync(&hctl, dctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     SB_CUDA(cudaStreamSynchronize(st));
     return SB_OK;

@@ -19,11 +19,54 @@
 //     fixed tree -> deterministic, within the 1e-12 / 1e-5 scale tolerance.
 #pragma once
 
+#include <type_traits>
+#include <utility>
+
 #include "common.cuh"
 
 namespace sb {
 
 // ============================================================ epilogues
+// Optional epilogue hooks, detected at compile time:
+//   prepare()   per-launch setup in every CTA (e.g. scalars read from a solver's
+//               control block once, not per row);
+//   gather(off) the gathered operand computed on the fly instead of loaded from b
+//               (CG's search direction p = z + beta p, fused into the SpMV that
+//               consumes it).  Only the row-owning kernels (strict / stream / vector /
+//               ELL / SELL-P) honour it; the launchers reject it for the others.
+template <class E, class = void>
+struct epi_has_gather : std::false_type {};
+template <class E>
+struct epi_has_gather<E, std::void_t<decltype(std::declval<const E &>().gather(int64_t(0)))>>
+    : std::true_type {};
+template <class E, class = void>
+struct epi_has_prepare : std::false_type {};
+template <class E>
+struct epi_has_prepare<E, std::void_t<decltype(std::declval<E &>().prepare())>> : std::true_type {};
+
+// Epilogues that gather through a hook carry more live registers; such an epilogue may
+// ask the TMA-staged kernels for a minimum residency (kMinThreadsPerSM / R CTAs per SM)
+// so the register allocator keeps four 256-row CTAs resident.
+template <class E, class = void>
+struct epi_min_threads : std::integral_constant<int, 0> {};
+template <class E>
+struct epi_min_threads<E, std::void_t<decltype(E::kMinThreadsPerSM)>>
+    : std::integral_constant<int, E::kMinThreadsPerSM> {};
+template <class Epi>
+constexpr int epi_min_ctas(int R) {
+    return epi_min_threads<Epi>::value / R;  // 0 = unspecified (the compiler's own heuristic)
+}
+
+template <class Epi, class V>
+__device__ __forceinline__ V gather_b(const Epi &e, const V *__restrict__ b, int64_t off) {
+    if constexpr (epi_has_gather<Epi>::value) return e.gather(off);
+    else return __ldg(b + off);
+}
+template <class Epi>
+__device__ __forceinline__ void epi_prepare(Epi &e) {
+    if constexpr (epi_has_prepare<Epi>::value) e.prepare();
+}
+
 template <class V>
 struct EpiStore {
     static constexpr int N = 1;  // no reduction; N=1 only sizes the (unused) partial array
@@ -45,12 +88,13 @@ __global__ void __launch_bounds__(256) csr_strict_kernel(int64_t rows, const I *
                                                          const V *__restrict__ b, int64_t ldb,
                                                          Epi epi) {
     if (epi.skip()) return;
+    epi_prepare(epi);
     double part[Epi::N] = {};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows;
          i += (int64_t)gridDim.x * blockDim.x) {
         double acc = 0.0;
         for (int64_t k = rp[i]; k < (int64_t)rp[i + 1]; ++k)
-            acc = addd(acc, mulp(val[k], __ldg(b + (int64_t)ci[k] * ldb)));
+            acc = addd(acc, mulp(val[k], gather_b(epi, b, (int64_t)ci[k] * ldb)));
         epi.row(i, acc, part);
     }
     epi.finish(part);
@@ -108,13 +152,14 @@ __device__ __forceinline__ uint32_t stage_range(const T *g, int64_t lo, int64_t 
 }
 
 template <class V, class I, int R, class Epi>
-__global__ void __launch_bounds__(R) csr_stream_kernel(int64_t rows, int64_t nnz,
+__global__ void __launch_bounds__(R, epi_min_ctas<Epi>(R)) csr_stream_kernel(int64_t rows, int64_t nnz,
                                                        const I *__restrict__ rp,
                                                        const I *__restrict__ ci,
                                                        const V *__restrict__ val,
                                                        const V *__restrict__ b, int64_t ldb,
                                                        int nnz_cap, Epi epi) {
     if (epi.skip()) return;
+    epi_prepare(epi);
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ StreamMeta meta[2];
@@ -174,19 +219,22 @@ __global__ void __launch_bounds__(R) csr_stream_kernel(int64_t rows, int64_t nnz
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     vv[j] = sv[k + j - m.av];
-                    bb[j] = __ldg(b + (int64_t)sc[k + j - m.ac] * ldb);
+                    bb[j] = gather_b(epi, b, (int64_t)sc[k + j - m.ac] * ldb);
                 }
 #pragma unroll
                 for (int j = 0; j < 8; ++j) acc = addd(acc, mulp(vv[j], bb[j]));
             }
             if (k < ke) {
+                // branch-free tail: lanes past the row end re-read its last entry (an L1
+                // hit) and are masked at the ordered adds, so every gather of the row is
+                // in flight before the first add (a gather hook that computes on the
+                // loaded values would otherwise serialise one latency per entry)
                 V vv[8], bb[8];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    if (k + j < ke) {
-                        vv[j] = sv[k + j - m.av];
-                        bb[j] = __ldg(b + (int64_t)sc[k + j - m.ac] * ldb);
-                    }
+                    const int64_t kk = k + j < ke ? k + j : ke - 1;
+                    vv[j] = sv[kk - m.av];
+                    bb[j] = gather_b(epi, b, (int64_t)sc[kk - m.ac] * ldb);
                 }
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
@@ -209,6 +257,7 @@ __global__ void __launch_bounds__(256) csr_vector_kernel(int64_t rows, const I *
                                                          const V *__restrict__ b, int64_t ldb,
                                                          Epi epi) {
     if (epi.skip()) return;
+    epi_prepare(epi);
     double part[Epi::N] = {};
     const int lane = threadIdx.x % S;
     const int64_t group = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / S;
@@ -229,12 +278,12 @@ __global__ void __launch_bounds__(256) csr_vector_kernel(int64_t rows, const I *
                     v[u] = ld_stream(val + k + u * S);
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) g[u] = __ldg(b + (int64_t)c[u] * ldb);
+                for (int u = 0; u < 4; ++u) g[u] = gather_b(epi, b, (int64_t)c[u] * ldb);
 #pragma unroll
                 for (int u = 0; u < 4; ++u) acc = addd(acc, mulp(v[u], g[u]));
             }
             for (; k < ke; k += S)
-                acc = addd(acc, mulp(ld_stream(val + k), __ldg(b + (int64_t)ld_stream(ci + k) * ldb)));
+                acc = addd(acc, mulp(ld_stream(val + k), gather_b(epi, b, (int64_t)ld_stream(ci + k) * ldb)));
         }
 #pragma unroll
         for (int o = S / 2; o > 0; o >>= 1) acc = addd(acc, __shfl_down_sync(0xffffffffu, acc, o, S));
@@ -637,8 +686,8 @@ __device__ __forceinline__ void load_column(const V *__restrict__ val, const I *
 // Accumulate `len` padded columns (column k at base0 + k*kstride) for RPT rows, four
 // columns per step with all loads and gathers issued before the ordered adds (padding
 // col = -1 is skipped, so each row's sum keeps the CSR order exactly).
-template <class V, class I, int RPT>
-__device__ __forceinline__ void padded_rows(const V *__restrict__ val, const I *__restrict__ col,
+template <class V, class I, int RPT, class Epi>
+__device__ __forceinline__ void padded_rows(const Epi &epi, const V *__restrict__ val, const I *__restrict__ col,
                                             const V *__restrict__ b, int64_t ldb, int64_t base0,
                                             int64_t kstride, int64_t len, double (&acc)[RPT]) {
     int64_t k = 0;
@@ -650,7 +699,8 @@ __device__ __forceinline__ void padded_rows(const V *__restrict__ val, const I *
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
-            for (int r = 0; r < RPT; ++r) gg[u][r] = cc[u][r] >= 0 ? __ldg(b + (int64_t)cc[u][r] * ldb) : (V)0;
+            for (int r = 0; r < RPT; ++r)  // padding gathers column 0 and is masked below
+                gg[u][r] = gather_b(epi, b, (int64_t)(cc[u][r] >= 0 ? cc[u][r] : 0) * ldb);
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -663,7 +713,7 @@ __device__ __forceinline__ void padded_rows(const V *__restrict__ val, const I *
         load_column<V, I, RPT>(val, col, base0 + k * kstride, vv, cc);
 #pragma unroll
         for (int r = 0; r < RPT; ++r)
-            if (cc[r] >= 0) acc[r] = addd(acc[r], mulp(vv[r], __ldg(b + (int64_t)cc[r] * ldb)));
+            if (cc[r] >= 0) acc[r] = addd(acc[r], mulp(vv[r], gather_b(epi, b, (int64_t)cc[r] * ldb)));
     }
 }
 
@@ -675,6 +725,7 @@ __global__ void __launch_bounds__(256) ell_kernel(int64_t rows, int64_t width, i
                                                   const I *__restrict__ col, const V *__restrict__ val,
                                                   const V *__restrict__ b, int64_t ldb, Epi epi) {
     if (epi.skip()) return;
+    epi_prepare(epi);
     double part[Epi::N] = {};
     const int64_t groups = (rows + RPT - 1) / RPT;
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < groups;
@@ -683,7 +734,7 @@ __global__ void __launch_bounds__(256) ell_kernel(int64_t rows, int64_t width, i
         double acc[RPT];
 #pragma unroll
         for (int r = 0; r < RPT; ++r) acc[r] = 0.0;
-        padded_rows<V, I, RPT>(val, col, b, ldb, i0, stride, width, acc);
+        padded_rows<V, I, RPT>(epi, val, col, b, ldb, i0, stride, width, acc);
 #pragma unroll
         for (int r = 0; r < RPT; ++r)
             if (i0 + r < rows) epi.row(i0 + r, acc[r], part);
@@ -702,6 +753,7 @@ __global__ void __launch_bounds__(256) sellp_kernel(int64_t rows, int64_t S,
                                                     const V *__restrict__ val,
                                                     const V *__restrict__ b, int64_t ldb, Epi epi) {
     if (epi.skip()) return;
+    epi_prepare(epi);
     double part[Epi::N] = {};
     const int64_t nslices = (rows + S - 1) / S;
     const int64_t groups = nslices * (S / RPT);
@@ -714,7 +766,7 @@ __global__ void __launch_bounds__(256) sellp_kernel(int64_t rows, int64_t S,
         double acc[RPT];
 #pragma unroll
         for (int r = 0; r < RPT; ++r) acc[r] = 0.0;
-        padded_rows<V, I, RPT>(val, col, b, ldb, off, S, len, acc);
+        padded_rows<V, I, RPT>(epi, val, col, b, ldb, off, S, len, acc);
 #pragma unroll
         for (int r = 0; r < RPT; ++r)
             if (i0 + r < rows) epi.row(i0 + r, acc[r], part);
@@ -746,6 +798,7 @@ __global__ void __launch_bounds__(128) sellp_stream_kernel(int64_t rows, int64_t
     constexpr int SPB = 128 / S;
     static_assert(SPB >= 1 && SPB <= 4, "slice size 32, 64 or 128");
     if (epi.skip()) return;
+    epi_prepare(epi);
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ SellpMeta meta[2];
@@ -814,7 +867,7 @@ __global__ void __launch_bounds__(128) sellp_stream_kernel(int64_t rows, int64_t
                     const int64_t e = o + (int64_t)(k + u) * S;
                     vv[u] = sv[dv + e];
                     cc[u] = sc[dc + e];
-                    bb[u] = cc[u] >= 0 ? __ldg(b + (int64_t)cc[u] * ldb) : (V)0;
+                    bb[u] = gather_b(epi, b, (int64_t)(cc[u] >= 0 ? cc[u] : 0) * ldb);  // padding: masked below
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
@@ -824,14 +877,11 @@ __global__ void __launch_bounds__(128) sellp_stream_kernel(int64_t rows, int64_t
                 V vv[8], bb[8];
                 I cc[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    cc[u] = (I)-1;
-                    if (k + u < len) {
-                        const int64_t e = o + (int64_t)(k + u) * S;
-                        vv[u] = sv[dv + e];
-                        cc[u] = sc[dc + e];
-                        if (cc[u] >= 0) bb[u] = __ldg(b + (int64_t)cc[u] * ldb);
-                    }
+                for (int u = 0; u < 8; ++u) {  // branch-free tail (see csr_stream_kernel)
+                    const int64_t e = o + (int64_t)(k + u < len ? k + u : len - 1) * S;
+                    vv[u] = sv[dv + e];
+                    cc[u] = k + u < len ? sc[dc + e] : (I)-1;
+                    bb[u] = gather_b(epi, b, (int64_t)(cc[u] >= 0 ? cc[u] : 0) * ldb);
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
@@ -850,6 +900,7 @@ template <class V, class Epi>
 __global__ void __launch_bounds__(256) epilogue_pass_kernel(int64_t rows, const V *x, int64_t ldx,
                                                             Epi epi) {
     if (epi.skip()) return;
+    epi_prepare(epi);
     double part[Epi::N] = {};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows;
          i += (int64_t)gridDim.x * blockDim.x)

@@ -155,6 +155,7 @@ cudaError_t csr_apply(const sb_csr &A, const V *b, int64_t ldb, V *x_out, int64_
         }
     }
     if (kernel == SB_CSR_MERGE) {
+        if constexpr (epi_has_gather<Epi>::value) return cudaErrorNotSupported;
         cudaError_t e = launch_csr_merge<V, I>(A, b, ldb, x_out, ldx, st);
         if (e != cudaSuccess || is_plain_store<Epi>::value) return e;
         return launch_epilogue_pass<V, I>(A.rows, x_out, ldx, epi, st);
@@ -196,6 +197,7 @@ cudaError_t coo_raw(const sb_coo &A, const V *b, int64_t ldb, V *x, int64_t ldx,
 template <class V, class I, class Epi>
 cudaError_t coo_apply(const sb_coo &A, const V *b, int64_t ldb, V *x_out, int64_t ldx,
                       const Epi &epi, cudaStream_t st) {
+    if constexpr (epi_has_gather<Epi>::value) return cudaErrorNotSupported;
     cudaError_t e = coo_raw<V, I>(A, b, ldb, x_out, ldx, false, st);
     if (e != cudaSuccess || is_plain_store<Epi>::value) return e;
     return launch_epilogue_pass<V, I>(A.rows, x_out, ldx, epi, st);
@@ -293,6 +295,7 @@ cudaError_t sellp_apply(const sb_sellp &A, const V *b, int64_t ldb, const Epi &e
 template <class V, class I, class Epi>
 cudaError_t hybrid_apply(const sb_hybrid &A, const V *b, int64_t ldb, V *x_out, int64_t ldx,
                          const Epi &epi, cudaStream_t st) {
+    if constexpr (epi_has_gather<Epi>::value) return cudaErrorNotSupported;
     cudaError_t e = ell_apply<V, I>(A.ell, b, ldb, EpiStore<V>{x_out, ldx}, st);
     if (e != cudaSuccess) return e;
     if (A.coo.nnz > 0) {
@@ -315,6 +318,20 @@ cudaError_t matrix_apply(const sb_matrix &M, const V *b, int64_t ldb, V *x_out, 
     case SB_FMT_HYBRID:
         return hybrid_apply<V, I>(*(const sb_hybrid *)M.mat, b, ldb, x_out, ldx, epi, st);
     default: return cudaErrorInvalidValue;
+    }
+}
+
+// Formats / kernels whose SpMV owns whole rows and so can evaluate a gathered operand
+// on the fly (epilogue gather hook): CSR strict / stream / vector, ELL, SELL-P.
+inline bool matrix_row_owning(const sb_matrix &M) {
+    switch (M.format) {
+    case SB_FMT_CSR: {
+        const sb_csr &A = *(const sb_csr *)M.mat;
+        return !A.plan || A.plan->kernel != SB_CSR_MERGE;
+    }
+    case SB_FMT_ELL:
+    case SB_FMT_SELLP: return true;
+    default: return false;
     }
 }
 

@@ -209,3 +209,68 @@ def test_config_solve_listing2(dev):
     del tree["krylov_dim"]
     log, _ = sp.config_solve(tree, dev, a, b, sp.dense_create(dev, a.rows, 1, sp.Precision.double, 0.0))
     assert log.converged
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_cg_fused_direction_bitwise(dev, dtype):
+    """The two-kernel CG loop (search direction evaluated inside the SpMV gather, x update
+    deferred to the next SpMV) reproduces the three-kernel loop bit for bit: same
+    iterations, residual history and solution, for every row-owning format and kernel,
+    odd and even final iterations, max_iters stops, x0 != 0, and without a
+    preconditioner; also in the polled (non-graph) loop."""
+    from paper_2510_08230_b200 import _lib
+    prec = sp.Precision.from_dtype(np.dtype(dtype))
+    a = gen.stencil_csr(dev, 18, dim=3, precision=prec)
+    rng = np.random.default_rng(5)
+    b = rng.random(a.rows).astype(dtype)
+    x0 = rng.random(a.rows).astype(dtype)
+    mats = [a, a.with_kernel("strict"), a.with_kernel("vector"), sp.ell_from_csr(a),
+            sp.sellp_from_csr(a), sp.coo_from_csr(a)]
+    cases = [([sp.Iteration(2000), sp.ResidualNorm(1e-7)], True, None),
+             ([sp.Iteration(7)], True, x0),             # odd max_iters stop
+             ([sp.Iteration(8)], False, None),          # even, identity preconditioner
+             ([sp.Iteration(2000), sp.ResidualNorm(1e-6)], False, x0)]
+    fn_fused, fn_graph = _lib.fn("sb_set_cg_fused"), _lib.fn("sb_set_graph_mode")
+    try:
+        for crit, pre, xi in cases:
+            runs = []
+            for fused, graph in ((0, 1), (1, 1), (2, 1), (1, 0), (2, 0)):
+                fn_fused(fused)
+                fn_graph(graph)
+                for k, mat in enumerate(mats):
+                    log, x, _ = solve(dev, "cg", mat, b, crit, precond=sp.jacobi_create(a) if pre else False,
+                                      x0=xi)
+                    runs.append((k, fused, graph, log, x))
+            for name, fused, graph, log, x in runs[len(mats):]:
+                ref = runs[name]  # same matrix / kernel, three-kernel graph loop
+                assert log.iterations == ref[3].iterations, (name, fused, graph)
+                assert log.residual_history == ref[3].residual_history, (name, fused, graph)
+                np.testing.assert_array_equal(x, ref[4], err_msg=f"{name} fused={fused} graph={graph}")
+    finally:
+        fn_fused(1)
+        fn_graph(1)
+
+
+@pytest.mark.parametrize("kind", ["cg", "cgs", "bicgstab", "gmres"])
+def test_graph_cache_tracks_workspace_layout(dev, kind):
+    """A captured solver loop is reused only for the same buffers: the workspace's vector
+    offsets depend on the history capacity (max_iters), so two solves with the same
+    pointers but different criteria must not share a graph (regression: a stale graph
+    iterated on the previous solve's vector offsets when x0 != 0)."""
+    a = gen.stencil_csr(dev, 16, dim=3)
+    rng = np.random.default_rng(11)
+    b, x0 = rng.random(a.rows), rng.random(a.rows)
+    rp, ci, v = (t.cpu().numpy() for t in (a.row_ptrs, a.col_idxs, a.values))
+    inv = sbref.jacobi_create(rp, ci, v)[0]
+    kw = {"krylov_dim": 30} if kind == "gmres" else {}
+    for crit, its in (([sp.Iteration(3000), sp.ResidualNorm(1e-8)], 3000), ([sp.Iteration(5)], 5),
+                      ([sp.Iteration(40)], 40)):
+        for _ in range(2):  # the second solve hits the graph cache with recycled buffers
+            log, x, _ = solve(dev, kind, a, b, crit, x0=x0, **kw)
+        ref, xr = sbref.solve(kind, rp, ci, v, b, x0=x0, inv_diag=inv, max_iters=its,
+                              reduction_factor=1e-8 if its == 3000 else None, **kw)
+        n = min(4, len(ref.residual_history))
+        np.testing.assert_allclose(log.residual_history[:n], ref.residual_history[:n], rtol=1e-9,
+                                   err_msg=f"{kind} max_iters={its}")
+        if its < 3000:
+            assert log.iterations == its
