@@ -205,6 +205,19 @@ def _spmv_roofline(a, dev, stream, torch, sp):
         "alg_bytes_per_launch": spmv_bytes, "peak_source": peak_kind}
 
 
+def _persistent_traffic(iter_bytes):
+    """DRAM bytes per CG iteration of the persistent kernel from the committed ncu
+    --set full capture (profiles/), if it was taken for this byte model."""
+    try:
+        with open(os.path.join(REPO, "profiles", "r1_cg_persistent_traffic.json")) as fh:
+            t = json.load(fh)
+        if t["algorithmic_bytes_per_iteration"] == iter_bytes:
+            return t["traffic_per_iteration"]
+    except Exception:
+        pass
+    return None
+
+
 def run_ours(args):
     import torch
 
@@ -253,10 +266,31 @@ def run_ours(args):
     ms = ev0.elapsed_time(ev1)
     value = iters / (ms / 1000.0)
 
-    spmv_ms, spmv_bytes, roofline = _spmv_roofline(a, dev, stream, torch, sp)
-    peak = roofline["peak"]
-    cg_iter_bytes = (12 * nnz + 4 * (n + 1)) + 13 * 8 * n
+    from paper_2510_08230_b200 import _lib
+    loop = int(_lib.fn("sb_cg_last_loop")())  # 3 persistent kernel, 1 fused graph, 0 three-kernel
+    spmv_ms, spmv_bytes, spmv_roof = _spmv_roofline(a, dev, stream, torch, sp)
+    peak = spmv_roof["peak"]
+    # algorithmic bytes of one iteration (SURVEY.md 8d / DESIGN.md 3): matrix once, plus
+    # 12 vector passes for the fused loops (gather z, p_old; write q, p; read p, q, x, r, M;
+    # write x, r, z), 13 for the three-kernel loop
+    a_bytes = 12 * nnz + 4 * (n + 1)
+    cg_iter_bytes = a_bytes + (13 if loop == 0 else 12) * 8 * n
     cg_iter_ms = ms / max(iters, 1)
+    if loop == 3:
+        # dominant kernel = the persistent CG kernel (one launch per solve, >99% of the
+        # step); its duration is taken as the whole solve (setup SpMV + init included)
+        achieved = cg_iter_bytes / (cg_iter_ms / 1e3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": _persistent_traffic(cg_iter_bytes),
+                    "kernel": "cg_persistent_kernel<double,int,256>",
+                    "alg_bytes_per_launch": cg_iter_bytes * log.iterations,
+                    "launch_us": ms / args.steps * 1e3, "peak_source": spmv_roof["peak_source"],
+                    "note": "bytes per launch = iterations x (matrix + 12 vector passes); "
+                            "traffic per iteration from the committed ncu capture"}
+        launches = args.steps * 3
+    else:
+        roofline = spmv_roof
+        launches = args.steps * (2 + (4 * ((log.iterations + 1) // 2) if loop == 1 else 3 * log.iterations))
 
     # ---- e2e: public frontend API with host buffers (pinned), copies inside the region
     pdev = pg.device("cuda", local)
@@ -301,13 +335,16 @@ def run_ours(args):
         "cg_iteration": {"ms": cg_iter_ms, "alg_bytes": cg_iter_bytes,
                          "gbs": cg_iter_bytes / (cg_iter_ms / 1e3) / 1e9,
                          "frac_of_hbm": cg_iter_bytes / (cg_iter_ms / 1e3) / 1e9 / peak},
-        "spmv": {"kernel": a.kernel, "us": spmv_ms * 1e3, "gbs": roofline["achieved"],
-                 "gflops": 2 * nnz / (spmv_ms / 1e3) / 1e9},
+        "cg_loop": {3: "persistent cooperative kernel", 1: "graph loop, fused direction",
+                    0: "graph loop, three kernels"}.get(loop, str(loop)),
+        "spmv": {"kernel": a.kernel, "us": spmv_ms * 1e3, "gbs": spmv_roof["achieved"],
+                 "gflops": 2 * nnz / (spmv_ms / 1e3) / 1e9, "roofline_frac": spmv_roof["frac"],
+                 "traffic": spmv_roof["traffic"]},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "CG iters/s", "h2d_bytes_per_step": 2 * 8 * n,
                 "d2h_bytes_per_step": 8 * n + 64},
-        "gpu_launches": args.steps * (2 + 3 * log.iterations),
+        "gpu_launches": launches,
         "clocks": clocks.summary(),
     }
     print(json.dumps(line))

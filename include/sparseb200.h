@@ -183,10 +183,15 @@ int sb_version(void);
 const char *sb_status_string(int code);
 /* CUDA graph + conditional-node solver loop (1, default) or host-polled launches (0) */
 void sb_set_graph_mode(int enabled);
-/* CG loop shape: 1 (default) = two kernels per iteration, the search direction evaluated
-   inside the SpMV gather (row-owning formats); 0 = three kernels (SpMV+dot, update,
-   direction).  Both produce bitwise identical iterates. */
-void sb_set_cg_fused(int enabled);
+/* CG loop shape: 3 (default) = one persistent cooperative kernel per solve for TMA-stream
+   CSR matrices up to 24 MB per vector, else 1; 1 = CUDA-graph loop of two kernels per
+   iteration, the search direction evaluated inside the SpMV gather (row-owning formats);
+   0 = three kernels per iteration (SpMV+dot, update, direction).  Modes 0 and 1 give
+   bitwise identical iterates; 3 differs only in the summation order of the dots. */
+void sb_set_cg_fused(int mode);
+/* Loop shape used by this thread's last CG solve: 0 three-kernel graph loop, 1 fused-
+   direction graph loop, 3 persistent cooperative kernel (one launch per solve). */
+int sb_cg_last_loop(void);
 
 #define SB_VALUE_DECLS(VN)                                                                       \
     /* core.dot / norm2 / axpy / scal / copy_into (core.py:358-401); jacobi apply (precond.py:57-63) */ \

@@ -164,6 +164,7 @@ _PLAIN_PROTOS = {
     "sb_status_string": (ctypes.c_char_p, [c_i32]),
     "sb_set_graph_mode": (None, [c_i32]),
     "sb_set_cg_fused": (None, [c_i32]),
+    "sb_cg_last_loop": (c_i32, []),
     "sb_csr_plan_select": (c_i32, [P(SbRowStats), c_i32, c_i32, c_i32, P(SbCsrPlan),
                                    P(SbError)]),
     "sb_coo_tile_entries": (c_i64, []),

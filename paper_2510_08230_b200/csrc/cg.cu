@@ -2,6 +2,7 @@
 #include <cmath>
 #include <atomic>
 #include <cstdlib>
+#include <vector>
 
 #include "solver_common.cuh"
 
@@ -132,98 +133,368 @@ struct CgDirection : SkipNone {
 // the fly at every gathered column, so p_k is never a separate pass: the epilogue
 // stores q = A p_k and the row's own p_k (ping-pong buffers: iteration k reads
 // buf[(k-1)&1] and writes buf[k&1], so no CTA overwrites a value another CTA still
-// gathers), accumulates p_k.q, and applies the PREVIOUS iteration's x += alpha p_{k-1}
-// (deferred from the update kernel, which then streams only r, q, M: r -= alpha q,
-// z = M r, r.r, r.z).  The x update of the final iteration is applied after the loop
-// (cg_xfinal_kernel).  Per iteration: A + 11 V n bytes instead of A + 13 V n, and one
-// launch fewer; every value is bitwise what the three-kernel loop computes.
-template <class V, bool DeferX>
+// gathers) and accumulates p_k.q; the update kernel then reads p_k back for x.
+// Per iteration: A + 12 V n bytes instead of A + 13 V n, and one launch fewer; every
+// value is bitwise what the three-kernel loop computes.
+template <class V>
+__device__ __forceinline__ V cg_direction(bool first, double beta, V zc, V pc) {
+    return first ? zc : axpy_e(1.0, zc, scal_e(beta, pc));  // p = z + beta p (scal; axpy)
+}
+
+template <class V>
 struct EpiCgFused {
     static constexpr int N = 1;
     static constexpr int kMinThreadsPerSM = 1024;
-    V *q, *pnew, *x;
+    V *q, *pnew;
     const V *z, *pold;
     Ctl *ctl;
     double *partials;
-    double beta, alpha;
+    double beta;
     int first;
     __device__ __forceinline__ bool skip() const { return loop_done(ctl); }
     __device__ __forceinline__ void prepare() {
         // read before any CTA of this launch can finish (the last CTA, which rewrites
-        // iter / alpha, starts its finalisation only after every CTA has arrived)
+        // iter, starts its finalisation only after every CTA has arrived)
         first = ctl->iter == 0;
         beta = ctl->beta;
-        alpha = ctl->alpha;
     }
     __device__ __forceinline__ V gather(int64_t c) const {
-        const V zc = __ldg(z + c);
-        return first ? zc : axpy_e(1.0, zc, scal_e(beta, __ldg(pold + c)));
+        return cg_direction(first, beta, __ldg(z + c), __ldg(pold + c));
     }
     __device__ __forceinline__ void row(int64_t i, double acc, double (&part)[N]) const {
         const V qi = (V)acc;
         q[i] = qi;
         const V pi = gather(i);
         pnew[i] = pi;
-        if (DeferX && !first) x[i] = axpy_e(alpha, __ldg(pold + i), x[i]);
         part[0] = addd(part[0], mulp(pi, qi));
     }
     __device__ __forceinline__ void finish(double (&part)[N]) const {
         double tot[N];
-        if (grid_reduce<N>(part, partials, &ctl->ticket[0], tot) && threadIdx.x == 0) {
-            if (DeferX) ctl->xpend = 0;  // x += alpha_{k-1} p_{k-1} applied by every CTA above
+        if (grid_reduce<N>(part, partials, &ctl->ticket[0], tot) && threadIdx.x == 0)
             CgPqFin{}.last(ctl, tot);
-        }
     }
 };
 
-// r -= alpha q; z = M r; dots r.r, r.z -> criteria, beta (x deferred to the next SpMV)
-template <class V>
-struct CgUpdateR : SkipNone {
-    using value_type = V;
-    const V *q, *inv;
-    V *r, *z;
-    double alpha;
-    __device__ __forceinline__ void prepare(const Ctl *c) { alpha = c->alpha; }
-    template <int W>
-    __device__ __forceinline__ void elem(int64_t i, double (&part)[2]) const {
-        const auto Q = ldp<W>(q, i), D = ldp_or_one<W>(inv, i);
-        auto R = ldp<W>(r, i);
-        Pk<V, W> Z;
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-            R.v[w] = axpy_e(-alpha, Q.v[w], R.v[w]);
-            Z.v[w] = inv ? vmul(R.v[w], D.v[w]) : R.v[w];
-            part[0] = addd(part[0], mulp(R.v[w], R.v[w]));
-            part[1] = addd(part[1], mulp(R.v[w], Z.v[w]));
-        }
-        stp<W>(r, i, R);
-        stp<W>(z, i, Z);
-    }
-    __device__ __forceinline__ void last(Ctl *c, const double (&tot)[2]) const {
-        c->xpend = 1;  // this iteration's x += alpha p is owed (next SpMV or cg_xfinal_kernel)
-        CgUpdate<V>{}.last(c, tot);
-    }
+// ---------------------------------------------------------------- persistent CG
+// The whole iteration loop as ONE cooperative kernel (CSR, TMA-staged row blocks): every
+// CTA owns the row blocks bid, bid + G, ... for the SpMV *and* the vector updates, and
+// the two reductions of an iteration are grid barriers after which every CTA sums the
+// per-CTA partials in the same fixed order (deterministic, identical scalars in every
+// CTA, so all CTAs take the same stop decision).  Per iteration:
+//   A: q = A p_k with p_k = z + beta p_{k-1} gathered on the fly (as EpiCgFused), store
+//      q and the own p_k, partial p_k.q; when its blocks are done, the CTA already
+//      issues the TMA copy of its first block of the NEXT SpMV (the matrix is
+//      immutable), so the stream restarts without a ramp after the barriers;
+//   barrier -> alpha (breakdown test);
+//   B: own rows: x += alpha p_k, r -= alpha q, z = M r, partials r.r, r.z;
+//   barrier -> ||r||, history, criteria, beta.
+// Vectors written by other CTAs inside the launch are read with plain (L1-cached)
+// loads: the acquire side of every grid barrier invalidates the SM's L1 (CCTL.IVALL in
+// the SASS), so no line cached before the barrier survives it.  The arithmetic of every element is the reference's
+// (and the graph loop's); only the summation order of the dots differs.
+struct CgPArgs {
+    int64_t n, nnz;
+    const void *rp, *ci, *val, *inv;
+    void *x, *r, *z, *p0, *p1, *q;
+    Ctl *ctl;
+    double *partials;  // 3 G doubles: [p.q | r.r, r.z] (+ G arrival stamps when profiling)
+    unsigned long long *prof;  // optional: arrival stamps of barriers 10..27 (18 G) + CTA 0 releases
+    int nnz_cap;
 };
 
-// after the loop: the deferred x += alpha_k p_k of the last completed iteration k
-template <class V>
-__global__ void __launch_bounds__(256) cg_xfinal_kernel(int64_t n, const Ctl *c, const V *p0,
-                                                        const V *p1, V *x) {
-    if (!c->xpend) return;
-    const V *p = (c->iter & 1) ? p1 : p0;
-    const double alpha = c->alpha;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        x[i] = axpy_e(alpha, p[i], x[i]);
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
 }
 
-// fused-direction loop on (default) / off (the three-kernel loop; A/B and parity tests)
-// 2 = x update deferred into the next SpMV as well (A + 11 V n)
-static std::atomic<int> g_cg_fused{[] {
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Grid barrier over all CTAs of a cooperative launch: a monotonic 64-bit arrival counter
+// (reset per solve).  Thread 0 of each CTA arrives with a fire-and-forget release
+// reduction and polls with acquire loads until every CTA of this epoch has arrived;
+// the acquire also invalidates the SM's L1, the surrounding __syncthreads extend the
+// ordering to the whole CTA.
+__device__ __forceinline__ void grid_barrier(unsigned long long *count, unsigned long long target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(count) : "memory");
+        unsigned long long v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(count) : "memory");
+        } while (v < target);
+    }
+    __syncthreads();
+}
+
+// every CTA publishes its N partials, waits, then sums all G partials in index order
+template <int N, int R>
+__device__ __forceinline__ void grid_allreduce(double (&v)[N], double *partials, unsigned long long *count,
+                                               unsigned long long target, double (&tot)[N],
+                                               unsigned long long *stamps = nullptr) {
+    __shared__ double scratch[32][N];
+    __shared__ double s_tot[N];
+    block_reduce<N>(v, scratch);
+    const int G = gridDim.x;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) partials[k * G + blockIdx.x] = v[k];
+        if (stamps && target / G >= 10 && target / G < 28)  // arrival stamps of barriers 10..27
+            stamps[(target / G - 10) * G + blockIdx.x] = gtimer();
+    }
+    grid_barrier(count, target);
+    unsigned long long t_rel = 0;
+    if (stamps && blockIdx.x == 0 && threadIdx.x == 0) t_rel = gtimer();
+    double a[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) a[k] = 0.0;
+    constexpr int U = 4;  // independent loads in flight per thread (G <= U R covers 1024 CTAs)
+    for (int i0 = threadIdx.x; i0 < G; i0 += U * R) {
+        double t[N][U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int k = 0; k < N; ++k) t[k][u] = i0 + u * R < G ? __ldcg(partials + k * G + i0 + u * R) : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int k = 0; k < N; ++k) a[k] = addd(a[k], t[k][u]);
+    }
+    block_reduce<N>(a, scratch);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int k = 0; k < N; ++k) s_tot[k] = a[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < N; ++k) tot[k] = s_tot[k];
+    if (stamps && blockIdx.x == 0 && threadIdx.x == 0 && target / G >= 10 && target / G < 28)
+        stamps[18 * G + (target / G - 10)] = t_rel;  // CTA 0's release time
+}
+
+template <class V, class I, int R>
+__global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ StreamMeta meta[2];
+    Ctl *c = a.ctl;
+    if (c->done) return;  // setup found the exact solution
+    const I *rp = (const I *)a.rp, *ci = (const I *)a.ci;
+    const V *val = (const V *)a.val, *inv = (const V *)a.inv;
+    V *x = (V *)a.x, *r = (V *)a.r, *z = (V *)a.z, *q = (V *)a.q;
+    const int64_t n = a.n, nnz = a.nnz;
+    const StreamLayout<V, I> L(R, a.nnz_cap);
+    const size_t sb = L.stage_bytes();
+    const int tid = threadIdx.x;
+    const int G = gridDim.x;
+    const int64_t nblk = (n + R - 1) / R;
+    const int64_t bid = blockIdx.x;
+    const uint64_t pol = policy_evict_first();
+    unsigned long long *count = &c->barrier;
+    unsigned long long epoch = 0;  // barriers passed in this launch
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    auto issue = [&](int64_t blk, int s) {  // thread 0 only (as csr_stream_kernel)
+        unsigned char *st = smem + s * sb;
+        V *sv = reinterpret_cast<V *>(st);
+        I *sc = reinterpret_cast<I *>(st + L.off_c());
+        I *sr = reinterpret_cast<I *>(st + L.off_r());
+        const int64_t r0 = blk * R, r1 = r0 + R < n ? r0 + R : n;
+        const int64_t k0 = rp[r0], k1 = rp[r1];
+        StreamMeta m;
+        m.r0 = r0;
+        m.r1 = r1;
+        uint32_t bv = stage_range(val, k0, k1, nnz, sv, m.av);
+        uint32_t bc = stage_range(ci, k0, k1, nnz, sc, m.ac);
+        uint32_t br = stage_range(rp, r0, r1 + 1, n + 1, sr, m.ar);
+        meta[s] = m;
+        mbar_arrive_expect_tx(&bar[s], bv + bc + br);
+        if (bv) bulk_g2s(sv, val + m.av, bv, &bar[s], pol);
+        if (bc) bulk_g2s(sc, ci + m.ac, bc, &bar[s], pol);
+        if (br) bulk_g2s(sr, rp + m.ar, br, &bar[s], pol);
+    };
+    uint32_t seq = 0;  // ring position: stage seq & 1, parity (seq >> 1) & 1
+    if (tid == 0 && bid < nblk) issue(bid, 0);
+
+    int64_t it = c->iter;
+    double rz = c->rz, beta = 0.0;
+    const double bnorm = c->bnorm;
+    bool first = true;
+    V *pold = (V *)a.p0, *pnew = (V *)a.p1;
+    unsigned long long tp[4] = {0, 0, 0, 0}, t0 = gtimer(), t1;
+    for (;;) {
+        // ---- A: q = A p_k, p_k = z + beta p_{k-1} gathered on the fly
+        double part[1] = {0.0};
+        for (int64_t blk = bid; blk < nblk; blk += G, ++seq) {
+            const int s = seq & 1;
+            const int64_t nxt = blk + G < nblk ? blk + G : bid;  // wrap: next SpMV's first block
+            if (tid == 0) issue(nxt, s ^ 1);
+            mbar_wait(&bar[s], (seq >> 1) & 1);
+            const unsigned char *st = smem + s * sb;
+            const V *sv = reinterpret_cast<const V *>(st);
+            const I *sc = reinterpret_cast<const I *>(st + L.off_c());
+            const I *sr = reinterpret_cast<const I *>(st + L.off_r());
+            const StreamMeta m = meta[s];
+            const int64_t i = m.r0 + tid;
+            if (i < m.r1) {
+                const int64_t kb = sr[i - m.ar], ke = sr[i + 1 - m.ar];
+                double acc = 0.0;
+                for (int64_t k = kb; k < ke; k += 8) {
+                    V vv[8], bb[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int64_t kk = k + j < ke ? k + j : ke - 1;
+                        const int64_t col = (int64_t)sc[kk - m.ac];
+                        vv[j] = sv[kk - m.av];
+                        bb[j] = cg_direction(first, beta, z[col], pold[col]);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        if (k + j < ke) acc = addd(acc, mulp(vv[j], bb[j]));
+                }
+                const V qi = (V)acc;
+                const V pi = cg_direction(first, beta, z[i], pold[i]);
+                q[i] = qi;
+                pnew[i] = pi;
+                part[0] = addd(part[0], mulp(pi, qi));
+            }
+            __syncthreads();  // stage s consumed before it is re-issued
+        }
+        t1 = gtimer();
+        tp[0] += t1 - t0;
+        t0 = t1;
+        double pq[1];
+        grid_allreduce<1, R>(part, a.partials, count, ++epoch * G, pq, a.prof);
+        t1 = gtimer();
+        tp[1] += t1 - t0;
+        t0 = t1;
+        ++it;
+        if (!isfinite(pq[0]) || pq[0] <= kBreakdownRtol * fabs(rz)) {
+            if (bid == 0 && tid == 0) breakdown(c, it);
+            break;
+        }
+        const double alpha = rz / pq[0];
+        // ---- B: x += alpha p_k; r -= alpha q; z = M r; r.r, r.z on the rows of this CTA's
+        // own SpMV blocks (same moving window over memory as phase A; measured faster than
+        // a balanced contiguous split, which scatters the accesses over the whole vectors)
+        double part2[2] = {0.0, 0.0};
+        for (int64_t blk = bid; blk < nblk; blk += G) {
+            const int64_t i = blk * R + tid;
+            if (i < n) {
+                const V pi = pnew[i], qi = q[i];
+                x[i] = axpy_e(alpha, pi, x[i]);
+                const V ri = axpy_e(-alpha, qi, r[i]);
+                const V zi = inv ? vmul(ri, inv[i]) : ri;
+                r[i] = ri;
+                z[i] = zi;
+                part2[0] = addd(part2[0], mulp(ri, ri));
+                part2[1] = addd(part2[1], mulp(ri, zi));
+            }
+        }
+        t1 = gtimer();
+        tp[2] += t1 - t0;
+        t0 = t1;
+        double tot[2];
+        grid_allreduce<2, R>(part2, a.partials + G, count, ++epoch * G, tot, a.prof);
+        t1 = gtimer();
+        tp[3] += t1 - t0;
+        t0 = t1;
+        const double rnorm = sqrt(tot[0]);
+        int reason = check_criteria(c, it, rnorm, bnorm);
+        if (reason == STOP_NONE && rnorm == 0.0) reason = STOP_RESIDUAL;
+        if (bid == 0 && tid == 0) {
+            c->rnorm = rnorm;
+            record(c, it, rnorm);
+        }
+        if (reason != STOP_NONE) {
+            if (bid == 0 && tid == 0) finish_with(c, it, reason);
+            break;
+        }
+        if (!isfinite(tot[1]) || rz == 0.0) {
+            if (bid == 0 && tid == 0) breakdown(c, it);
+            break;
+        }
+        beta = tot[1] / rz;
+        rz = tot[1];
+        first = false;
+        V *t = pold;
+        pold = pnew;
+        pnew = t;
+    }
+    if (tid == 0 && bid < nblk) mbar_wait(&bar[seq & 1], (seq >> 1) & 1);  // drain the prefetch
+    if (bid == 0 && tid == 0) {
+        c->rz = rz;
+        c->beta = beta;
+        for (int k = 0; k < 4; ++k) c->tphase[k] = tp[k];
+        c->tphase[4] = G;
+    }
+}
+
+// Launch the persistent loop if the matrix is a stream-kernel CSR whose 256-row block
+// stage fits, and the grid can be co-resident (cooperative launch); false = not
+// applicable (the caller runs the graph loop).
+template <class V, class I>
+bool cg_persistent_launch(const sb_matrix &M, const CgPArgs &proto, cudaStream_t st, cudaError_t &err) {
+    constexpr int R = 256;
+    err = cudaSuccess;
+    if (M.format != SB_FMT_CSR) return false;
+    const sb_csr &A = *(const sb_csr *)M.mat;
+    if (!A.plan || A.plan->kernel != SB_CSR_STREAM || A.rows == 0) return false;
+    const int cap = A.plan->block_rows == 256 ? A.plan->nnz_cap
+                                              : (A.plan->block_rows == 128 ? A.plan->nnz_cap256 : 0);
+    if (cap <= 0) return false;
+    const size_t smem = 2 * StreamLayout<V, I>(R, cap).stage_bytes();
+    if (smem > 200 * 1024) return false;
+    auto kern = cg_persistent_kernel<V, I, R>;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        configured = true;
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, R, smem) != cudaSuccess || per_sm < 1) {
+        cudaGetLastError();
+        return false;
+    }
+    const int64_t nblk = ceil_div(A.rows, R);
+    int64_t grid = (int64_t)per_sm * device_info().sms;
+    if (grid > nblk) grid = nblk;
+    if (grid > kMaxGrid) grid = kMaxGrid;
+    CgPArgs args = proto;
+    args.n = A.rows;
+    args.nnz = A.nnz;
+    args.rp = A.row_ptrs;
+    args.ci = A.col_idxs;
+    args.val = A.values;
+    args.nnz_cap = cap;
+    void *params[] = {&args};
+    err = cudaLaunchCooperativeKernel((const void *)kern, dim3((unsigned)grid), dim3(R), params, smem, st);
+    if (err != cudaSuccess) {
+        cudaGetLastError();
+        return false;  // not co-resident here: graph loop instead
+    }
+    return true;
+}
+
+// CG loop shape: 3 = persistent kernel where applicable (default), else the graph loop
+// with the fused direction (1) or the three-kernel loop (0).  Measured per iteration on
+// B200 (tools/cg_modes.py, fp64 Poisson, us): p=64 25.6 / 22.2 / 14.8, p=96 41.9 / 38.0 /
+// 29.6, p=128 79.1 / 73.8 / 72.1, p=160 147 / 134 / 138, p=256 557 / 526 / 554 for
+// modes 0 / 1 / 3: the persistent loop wins while its two grid barriers per iteration
+// are a large share, the fused graph loop beyond ~24 MB per vector.
+static std::atomic<int> g_cg_mode{[] {
     const char *e = getenv("SPARSEB200_CG_FUSED");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 3;
 }()};
-inline bool cg_fused_enabled() { return g_cg_fused.load() != 0; }
+constexpr size_t kPersistentMaxVectorBytes = 24u << 20;
+static thread_local int g_cg_last_loop = -1;  // loop shape of this thread's last CG solve
 
 template <class V, class I>
 sb_status cg_solve(const SolveArgs &a) {
@@ -241,61 +512,94 @@ sb_status cg_solve(const SolveArgs &a) {
     double *part = w.partials;
     const sb_matrix M = *a.A;
     Ctl h = initial_ctl(*a.crit, w, cap);
+    const int mode = g_cg_mode.load();
+    const bool fused = mode != 0 && matrix_row_owning(M);
+    auto setup = [=](cudaStream_t st) -> cudaError_t {
+        cudaError_t e = matrix_apply<V, I>(M, x, 1, t, 1, EpiStore<V>{t, 1}, st);
+        if (e != cudaSuccess) return e;
+        return launch_ew<3>(n, ctl, part, CgInit<V>{{}, b, t, inv, r, z, fused ? nullptr : p}, st);
+    };
+    if (mode == 3 && fused && (size_t)n * sizeof(V) <= kPersistentMaxVectorBytes) {
+        // one cooperative launch runs every iteration; p ping-pongs between p and t
+        h.cond = 0ull;
+        SB_CUDA(cudaMemcpyAsync(ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, a.st));
+        SB_CUDA(setup(a.st));
+        CgPArgs pa = {};
+        pa.inv = inv;
+        pa.x = x;
+        pa.r = r;
+        pa.z = z;
+        pa.p0 = p;
+        pa.p1 = t;
+        pa.q = q;
+        pa.ctl = ctl;
+        pa.partials = part;
+        static const bool prof = getenv("SPARSEB200_CG_PROFILE") != nullptr;
+        pa.prof = prof ? reinterpret_cast<unsigned long long *>(part + 4096) : nullptr;  // G <= 1000
+        cudaError_t le;
+        if (cg_persistent_launch<V, I>(M, pa, a.st, le)) {
+            g_cg_last_loop = 3;
+            SB_CUDA(cudaMemcpyAsync(&h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, a.st));
+            SB_CUDA(cudaStreamSynchronize(a.st));
+            if (prof && h.iter > 0)
+                fprintf(stderr, "[sparseb200] persistent CG %lld it: A %.2f | bar1 %.2f | B %.2f | bar2 %.2f us/it\n",
+                        (long long)h.iter, h.tphase[0] * 1e-3 / h.iter, h.tphase[1] * 1e-3 / h.iter,
+                        h.tphase[2] * 1e-3 / h.iter, h.tphase[3] * 1e-3 / h.iter);
+            if (prof && h.iter > 14) {  // per barrier: arrival spread, CTA-0 wait, wake-up
+                const int G = (int)h.tphase[4];
+                std::vector<unsigned long long> st(19 * (size_t)G);
+                SB_CUDA(cudaMemcpy(st.data(), pa.prof, st.size() * 8, cudaMemcpyDeviceToHost));
+                for (int e = 0; e < 18 && 10 + e <= 2 * h.iter; ++e) {
+                    unsigned long long lo = ~0ull, hi = 0;
+                    int slow = 0;
+                    for (int i = 0; i < G; ++i) {
+                        const unsigned long long t = st[(size_t)e * G + i];
+                        if (t < lo) lo = t;
+                        if (t > hi) { hi = t; slow = i; }
+                    }
+                    fprintf(stderr, "[sparseb200]   barrier %d: spread %.2f us (slowest CTA %d), CTA0 waits %.2f, wake %.2f\n",
+                            10 + e, (hi - lo) * 1e-3, slow, (hi - st[(size_t)e * G]) * 1e-3,
+                            ((long long)st[18 * (size_t)G + e] - (long long)hi) * 1e-3);
+                }
+            }
+            return finish_log(h, a, w);
+        }
+        // not applicable: fall through to the graph loop (setup is re-run by run_loop)
+    }
     LoopSpec spec;
     spec.key = "cg" + std::to_string(sizeof(V)) + std::to_string(sizeof(I)) + "|" + matrix_key(M) +
                ptr_key({a.inv, b, x, a.ws, w.vecs, w.hist, w.small});
     spec.poll_chunk = 8;
     spec.hot_base = r;  // r, z, p, q, t are contiguous in the workspace
     spec.hot_bytes = 5 * w.vec_bytes;
-    const bool fused = cg_fused_enabled() && matrix_row_owning(M);
-    spec.setup = [=](cudaStream_t st) -> cudaError_t {
-        cudaError_t e = matrix_apply<V, I>(M, x, 1, t, 1, EpiStore<V>{t, 1}, st);
-        if (e != cudaSuccess) return e;
-        return launch_ew<3>(n, ctl, part, CgInit<V>{{}, b, t, inv, r, z, fused ? nullptr : p}, st);
-    };
+    spec.setup = setup;
     if (fused) {
         // p ping-pongs between p (buf 0) and t (buf 1; free once setup consumed A x0);
         // one body = an odd and an even iteration, so the buffer roles stay fixed
         spec.key += "|fused";
         spec.poll_chunk = 4;
-        const bool defer_x = g_cg_fused.load() == 2;
-        spec.key += defer_x ? "x" : "";
         spec.body = [=](cudaStream_t st) -> cudaError_t {
             for (int h = 0; h < 2; ++h) {
                 V *pold = h == 0 ? p : t, *pnew = h == 0 ? t : p;
-                cudaError_t e;
-                if (defer_x) {
-                    e = matrix_apply<V, I>(
-                        M, pold, 1, q, 1, EpiCgFused<V, true>{q, pnew, x, z, pold, ctl, part, 0.0, 0.0, 0}, st);
-                    if (e != cudaSuccess) return e;
-                    e = launch_ew<2>(n, ctl, part, CgUpdateR<V>{{}, q, inv, r, z, 0.0}, st);
-                } else {
-                    e = matrix_apply<V, I>(
-                        M, pold, 1, q, 1, EpiCgFused<V, false>{q, pnew, x, z, pold, ctl, part, 0.0, 0.0, 0}, st);
-                    if (e != cudaSuccess) return e;
-                    e = launch_ew<2>(n, ctl, part, CgUpdate<V>{{}, pnew, q, inv, x, r, z, 0.0}, st);
-                }
+                cudaError_t e = matrix_apply<V, I>(
+                    M, pold, 1, q, 1, EpiCgFused<V>{q, pnew, z, pold, ctl, part, 0.0, 0}, st);
+                if (e != cudaSuccess) return e;
+                e = launch_ew<2>(n, ctl, part, CgUpdate<V>{{}, pnew, q, inv, x, r, z, 0.0}, st);
                 if (e != cudaSuccess) return e;
             }
             return cudaSuccess;
         };
-        if (defer_x)
-            spec.finish = [=](cudaStream_t st) -> cudaError_t {
-                cg_xfinal_kernel<V><<<solver_grid(), 256, 0, st>>>(n, ctl, p, t, x);
-                return cudaGetLastError();
-            };
-        s = run_loop(spec, ctl, h, a.st, err);
-        if (s != SB_OK) return s;
-        return finish_log(h, a, w);
+    } else {
+        spec.body = [=](cudaStream_t st) -> cudaError_t {
+            cudaError_t e = matrix_apply<V, I>(
+                M, p, 1, q, 1, EpiSolver<V, 1, CgPqFin>{q, p, nullptr, ctl, part, CgPqFin{}}, st);
+            if (e != cudaSuccess) return e;
+            e = launch_ew<2>(n, ctl, part, CgUpdate<V>{{}, p, q, inv, x, r, z, 0.0}, st);
+            if (e != cudaSuccess) return e;
+            return launch_ew<0>(n, ctl, part, CgDirection<V>{{}, z, p, 0.0}, st);
+        };
     }
-    spec.body = [=](cudaStream_t st) -> cudaError_t {
-        cudaError_t e = matrix_apply<V, I>(
-            M, p, 1, q, 1, EpiSolver<V, 1, CgPqFin>{q, p, nullptr, ctl, part, CgPqFin{}}, st);
-        if (e != cudaSuccess) return e;
-        e = launch_ew<2>(n, ctl, part, CgUpdate<V>{{}, p, q, inv, x, r, z, 0.0}, st);
-        if (e != cudaSuccess) return e;
-        return launch_ew<0>(n, ctl, part, CgDirection<V>{{}, z, p, 0.0}, st);
-    };
+    g_cg_last_loop = fused ? 1 : 0;
     s = run_loop(spec, ctl, h, a.st, err);
     if (s != SB_OK) return s;
     return finish_log(h, a, w);
@@ -308,7 +612,8 @@ using namespace sb;
 
 extern "C" {
 
-void sb_set_cg_fused(int mode) { g_cg_fused = mode; }
+void sb_set_cg_fused(int mode) { g_cg_mode = mode; }
+int sb_cg_last_loop(void) { return g_cg_last_loop; }
 
 #define SB_DEFS(V, VN, I, IN) \
     sb_status sb_cg_solve_##VN##_##IN(const sb_matrix *a, const void *inv_diag,                    \

@@ -56,7 +56,8 @@ struct Ctl {
     double hnorm, beta_restart;
     int64_t cycle;
     double dot[8];  // row-partitioned solves: local dot totals, reduced across ranks in place
-    int32_t xpend;  // fused CG: x += alpha p of the last completed iteration still pending
+    unsigned long long tphase[10];  // persistent CG: CTA 0's ns per phase, summed over iterations
+    unsigned long long barrier;    // persistent CG: grid-barrier arrivals (0 at every solve start)
 };
 static_assert(sizeof(Ctl) <= 4096, "control block must fit kCtlBytes");
 
@@ -159,6 +160,8 @@ inline int solver_grid() { return device_info().sms * 8; }
 
 template <int N, int W, class Op>
 __global__ void __launch_bounds__(256) ew_kernel(int64_t n, Ctl *ctl, double *partials, Op op) {
+    pdl_wait();
+    pdl_trigger();
     if (loop_done(ctl) || op.skip(ctl)) return;
     op.prepare(ctl);
     double part[N > 0 ? N : 1] = {};
@@ -178,8 +181,7 @@ __global__ void __launch_bounds__(256) ew_kernel(int64_t n, Ctl *ctl, double *pa
 template <int N, class Op>
 cudaError_t launch_ew(int64_t n, Ctl *ctl, double *partials, const Op &op, cudaStream_t st) {
     constexpr int W = 16 / sizeof(typename Op::value_type);
-    ew_kernel<N, W, Op><<<solver_grid(), 256, 0, st>>>(n, ctl, partials, op);
-    return cudaGetLastError();
+    return launch_pdl(ew_kernel<N, W, Op>, solver_grid(), 256, 0, st, n, ctl, partials, op);
 }
 
 // single-thread scalar step (host-free control logic between passes)
@@ -291,7 +293,6 @@ struct LoopSpec {
     std::string key;                                   // identifies the captured body
     std::function<cudaError_t(cudaStream_t)> setup;    // enqueued once before the loop
     std::function<cudaError_t(cudaStream_t)> body;     // one loop iteration (or GMRES cycle)
-    std::function<cudaError_t(cudaStream_t)> finish;   // enqueued once after the loop (optional)
     int poll_chunk;                                    // iterations per host poll (fallback)
     void *hot_base = nullptr;                          // L2-persisting window (work vectors)
     size_t hot_bytes = 0;

@@ -158,8 +158,6 @@ __global__ void __launch_bounds__(R, epi_min_ctas<Epi>(R)) csr_stream_kernel(int
                                                        const V *__restrict__ val,
                                                        const V *__restrict__ b, int64_t ldb,
                                                        int nnz_cap, Epi epi) {
-    if (epi.skip()) return;
-    epi_prepare(epi);
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ StreamMeta meta[2];
@@ -196,9 +194,18 @@ __global__ void __launch_bounds__(R, epi_min_ctas<Epi>(R)) csr_stream_kernel(int
         if (br) bulk_g2s(sr, rp + m.ar, br, &bar[s], pol);
     };
 
-    double part[Epi::N] = {};
+    // the first block's matrix ranges are immutable: their TMA copies are issued before
+    // waiting on the predecessor kernel (programmatic dependent launch)
     int64_t blk = blockIdx.x;
     if (tid == 0 && blk < nblk) issue(blk, 0);
+    pdl_wait();
+    pdl_trigger();
+    if (epi.skip()) {
+        if (tid == 0 && blk < nblk) mbar_wait(&bar[0], 0);  // no bulk copy outlives the CTA
+        return;
+    }
+    epi_prepare(epi);
+    double part[Epi::N] = {};
     for (int it = 0; blk < nblk; blk += gridDim.x, ++it) {
         const int s = it & 1;
         const uint32_t parity = (it >> 1) & 1;

@@ -51,9 +51,15 @@ cudaError_t launch_csr_stream(const sb_csr &A, const V *b, int64_t ldb, const Ep
     int grid = persistent_grid(kern, R, smem);
     const int64_t nblk = ceil_div(A.rows, R);
     if (grid > nblk) grid = (int)nblk;
-    kern<<<grid, R, smem, st>>>(A.rows, A.nnz, (const I *)A.row_ptrs, (const I *)A.col_idxs,
-                                (const V *)A.values, b, ldb, cap, epi);
-    return cudaGetLastError();
+    if (is_plain_store<Epi>::value) {  // standalone SpMV: ordinary stream serialisation
+        kern<<<grid, R, smem, st>>>(A.rows, A.nnz, (const I *)A.row_ptrs, (const I *)A.col_idxs,
+                                    (const V *)A.values, b, ldb, cap, epi);
+        return cudaGetLastError();
+    }
+    // inside solver loops: programmatic dependent launch (the matrix prefetch of the first
+    // block overlaps the predecessor's drain; its predecessors never write the matrix)
+    return launch_pdl(kern, grid, R, smem, st, A.rows, A.nnz, (const I *)A.row_ptrs,
+                      (const I *)A.col_idxs, (const V *)A.values, b, ldb, cap, epi);
 }
 
 template <class V, class I, int S, class Epi>

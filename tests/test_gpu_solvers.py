@@ -234,7 +234,7 @@ def test_cg_fused_direction_bitwise(dev, dtype):
     try:
         for crit, pre, xi in cases:
             runs = []
-            for fused, graph in ((0, 1), (1, 1), (2, 1), (1, 0), (2, 0)):
+            for fused, graph in ((0, 1), (1, 1), (1, 0), (0, 0)):
                 fn_fused(fused)
                 fn_graph(graph)
                 for k, mat in enumerate(mats):
@@ -247,8 +247,56 @@ def test_cg_fused_direction_bitwise(dev, dtype):
                 assert log.residual_history == ref[3].residual_history, (name, fused, graph)
                 np.testing.assert_array_equal(x, ref[4], err_msg=f"{name} fused={fused} graph={graph}")
     finally:
-        fn_fused(1)
+        fn_fused(3)
         fn_graph(1)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_cg_persistent_kernel(dev, dtype):
+    """The single-launch persistent CG (CSR stream matrices) against the graph loop and the
+    oracle: same iteration counts and stop reasons, residual histories equal up to the
+    dot-product summation order, same solutions to rounding; odd / even max_iters stops,
+    x0 != 0, identity preconditioner, breakdown and exact-solution exits."""
+    from paper_2510_08230_b200 import _lib
+    prec = sp.Precision.from_dtype(np.dtype(dtype))
+    a = gen.stencil_csr(dev, 24, dim=3, precision=prec)
+    rp, ci, v = (t.cpu().numpy() for t in (a.row_ptrs, a.col_idxs, a.values))
+    rng = np.random.default_rng(9)
+    b = rng.random(a.rows).astype(dtype)
+    x0 = rng.random(a.rows).astype(dtype)
+    inv = sbref.jacobi_create(rp, ci, v)[0]
+    rtol = 1e-9 if dtype == np.float64 else 1e-4
+    set_mode = _lib.fn("sb_set_cg_fused")
+    try:
+        for crit, pre, xi, its, rf in (([sp.Iteration(5000), sp.ResidualNorm(1e-7)], True, None, 5000, 1e-7),
+                                       ([sp.Iteration(7)], True, x0, 7, None),
+                                       ([sp.Iteration(8)], False, x0, 8, None),
+                                       ([sp.Iteration(5000), sp.ResidualNorm(1e-6)], False, None, 5000, 1e-6)):
+            logs = {}
+            for mode in (1, 3):
+                set_mode(mode)
+                logs[mode] = solve(dev, "cg", a, b, crit, precond=sp.jacobi_create(a) if pre else False, x0=xi)
+            ref, xr = sbref.solve("cg", rp, ci, v, b, x0=xi, inv_diag=inv if pre else None, max_iters=its,
+                                  reduction_factor=rf)
+            (l1, x1, _), (l3, x3, _) = logs[1], logs[3]
+            assert l3.iterations == l1.iterations or (rf and within(l3.iterations, ref.iterations))
+            assert l3.stop_reason == l1.stop_reason == ref.stop_reason
+            n = min(5, len(ref.residual_history))
+            np.testing.assert_allclose(l3.residual_history[:n], ref.residual_history[:n], rtol=rtol)
+            if rf is None:
+                np.testing.assert_allclose(x3, x1, rtol=rtol * 10, atol=rtol)
+            else:
+                assert l3.residual_history[-1] <= rf * np.linalg.norm(b.astype(np.float64)) * 1.0001
+        set_mode(3)
+        if dtype == np.float64:
+            zero = sp.csr_from_dense(dev, np.zeros((300, 300)), keep_zeros=False).with_kernel("stream")
+            with pytest.raises(sp.errors.BreakdownError) as exc:
+                solve(dev, "cg", zero, np.ones(300), [sp.Iteration(10)], precond=False)
+            assert exc.value.iteration == 1
+        exact, _, _ = solve(dev, "cg", a, np.zeros(a.rows, dtype), [sp.Iteration(10), sp.ResidualNorm(1e-6)])
+        assert exact.iterations == 0 and exact.converged
+    finally:
+        set_mode(3)
 
 
 @pytest.mark.parametrize("kind", ["cg", "cgs", "bicgstab", "gmres"])
