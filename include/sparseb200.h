@@ -82,7 +82,9 @@ enum {
     SB_CSR_STRICT = 1, /* thread per row, global loads: the reference loop on the device */
     SB_CSR_STREAM = 2, /* TMA-staged row blocks, thread per row (regular rows; bit-exact) */
     SB_CSR_VECTOR = 3, /* sub-warp per row (long regular rows) */
-    SB_CSR_MERGE = 4   /* load-balanced merge-path (irregular rows) */
+    SB_CSR_MERGE = 4,  /* load-balanced merge-path (irregular rows) */
+    SB_CSR_TILE = 5    /* fixed nnz tiles, TMA-staged, parallel gathers, per-row segment
+                          sums + deterministic carry records (irregular rows) */
 };
 
 typedef struct {
@@ -96,7 +98,9 @@ typedef struct {
     int32_t block_rows;     /* stream: rows per block R; vector: lanes per row */
     int32_t nnz_cap;        /* stream: max nnz of one R-row block */
     int32_t nnz_cap256;     /* stream: max nnz of one 256-row block (solver epilogues) */
-    int64_t num_tiles;      /* merge: tiles of items_per_tile merge items */
+    int64_t num_tiles;      /* merge: tiles of items_per_tile merge items;
+                               tile: 2 x ceil(nnz / items_per_tile) carry records
+                               (tile_rows = first row of every tile, tile_nnz unused) */
     int64_t items_per_tile;
     void *tile_rows;        /* merge: int64[num_tiles + 1] */
     void *tile_nnz;         /* merge: int64[num_tiles + 1] */

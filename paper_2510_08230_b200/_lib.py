@@ -104,9 +104,9 @@ class SbDistPart(ctypes.Structure):
 
 
 FMT_CSR, FMT_COO, FMT_ELL, FMT_SELLP, FMT_HYBRID = 0, 1, 2, 3, 4
-CSR_AUTO, CSR_STRICT, CSR_STREAM, CSR_VECTOR, CSR_MERGE = 0, 1, 2, 3, 4
+CSR_AUTO, CSR_STRICT, CSR_STREAM, CSR_VECTOR, CSR_MERGE, CSR_TILE = 0, 1, 2, 3, 4, 5
 CSR_KERNELS = {"auto": CSR_AUTO, "strict": CSR_STRICT, "stream": CSR_STREAM,
-               "vector": CSR_VECTOR, "merge": CSR_MERGE}
+               "vector": CSR_VECTOR, "merge": CSR_MERGE, "tile": CSR_TILE}
 SOLVER_CG, SOLVER_CGS, SOLVER_GMRES, SOLVER_BICGSTAB = 0, 1, 2, 3
 
 P = ctypes.POINTER

@@ -113,7 +113,7 @@ sb_status plan_select(const sb_row_stats *S, int vbytes, int ibytes, int force, 
     if (kernel == SB_CSR_AUTO) {
         const bool irregular = (double)S->max_len > 8.0 * mean + 64.0;
         if (S->rows == 0 || S->nnz == 0) kernel = SB_CSR_STRICT;
-        else if (irregular) kernel = SB_CSR_MERGE;
+        else if (irregular) kernel = SB_CSR_TILE;
         else if (stream_R && mean <= 48.0) kernel = SB_CSR_STREAM;
         else kernel = SB_CSR_VECTOR;
     }
@@ -135,6 +135,9 @@ sb_status plan_select(const sb_row_stats *S, int vbytes, int ibytes, int force, 
     } else if (kernel == SB_CSR_MERGE) {
         P->items_per_tile = kMergeNT * kMergeIPT;
         P->num_tiles = ceil_div(S->rows + S->nnz, P->items_per_tile);
+    } else if (kernel == SB_CSR_TILE) {
+        P->items_per_tile = tile_nnz_default();
+        P->num_tiles = 2 * ceil_div(S->nnz, P->items_per_tile);  // lead + trail record per tile
     }
     return SB_OK;
 }
@@ -143,9 +146,16 @@ template <class I>
 sb_status plan_build(int64_t rows, int64_t nnz, const void *rp, sb_csr_plan *P, cudaStream_t st,
                      sb_error *err) {
     if (!P) return fail(err, SB_ERR_INVALID_ARGUMENT, "plan_build: null plan");
-    if (P->kernel != SB_CSR_MERGE || P->num_tiles == 0) return SB_OK;
+    if ((P->kernel != SB_CSR_MERGE && P->kernel != SB_CSR_TILE) || P->num_tiles == 0) return SB_OK;
     if (!P->tile_rows || !P->tile_nnz || !P->carry_rows || !P->carry_vals)
-        return fail(err, SB_ERR_INVALID_ARGUMENT, "merge plan buffers not allocated");
+        return fail(err, SB_ERR_INVALID_ARGUMENT, "merge / tile plan buffers not allocated");
+    if (P->kernel == SB_CSR_TILE) {
+        const int64_t nt = P->num_tiles / 2;
+        tile_partition_kernel<I><<<(int)ceil_div(nt + 1, 256), 256, 0, st>>>(
+            rows, (const I *)rp, P->items_per_tile, nt, (int64_t *)P->tile_rows);
+        SB_CUDA(cudaGetLastError());
+        return SB_OK;
+    }
     const int64_t n = P->num_tiles + 1;
     merge_path_partition_kernel<I><<<(int)ceil_div(n, 256), 256, 0, st>>>(
         rows, nnz, (const I *)rp, P->items_per_tile, P->num_tiles, (int64_t *)P->tile_rows,

@@ -480,6 +480,387 @@ __global__ void __launch_bounds__(NT) csr_merge_kernel(int64_t rows, const I *__
     }
 }
 
+// ============================================================ CSR: nnz tiles
+// Tile t = nonzeros [t C, (t+1) C): exactly C nonzeros per tile whatever the row lengths.
+// One elected thread TMA-copies the tile's values, columns and the row pointers of the
+// rows starting in it (first_row[t] .. first_row[t+1], known one tile ahead) into a
+// two-stage shared ring, the next tile prefetched; all threads then form the tile's
+// products with every gather of a thread in flight at once (random gathers are bound by
+// the L1/L2 sector rate, ~270 G/s on B200, tools/micro/gather_bench.cu) and store them
+// in place (an fp32 product is exact in fp32).  Rows starting in the tile are reduced
+// from shared memory: segments of <= 32 products by one thread in stored order (a row
+// wholly inside the tile is then bitwise the reference's sum), longer ones by a warp
+// (lane-strided partials, fixed shuffle tree).  A row crossing tile boundaries is not
+// written by any tile: its owner emits a "trail" record (row, first-segment sum) and
+// every later tile it reaches a "lead" record; tile_carry_fixup_kernel sums each row's
+// records in nnz order.  Deterministic, no atomics on values.
+struct TileMeta {
+    int64_t r0, r1;      // rows starting in the tile
+    int64_t dv, dc, dr;  // stage slot of the first value / column / row pointer
+    int32_t staged_rp;   // row pointers r0 .. r1 staged (else read from global)
+};
+
+template <class V, class I, int C, int RCAP>
+struct TileLayout {
+    static constexpr int VV = 16 / sizeof(V), VI = 16 / sizeof(I);
+    static constexpr size_t OFF_C = ((size_t)(C + 2 * VV) * sizeof(V) + 15) & ~size_t(15);
+    static constexpr size_t OFF_R = (OFF_C + (size_t)(C + 2 * VI) * sizeof(I) + 15) & ~size_t(15);
+    static constexpr size_t STAGE = (OFF_R + (size_t)(RCAP + 1 + 2 * VI) * sizeof(I) + 15) & ~size_t(15);
+};
+
+// Three-stage software pipeline, one block barrier per tile: iteration i issues the TMA
+// copy of tile i+1, issues the gathers of tile i, reduces the rows of tile i-1 (whose
+// products are in shared memory) while those gathers are in flight, then multiplies and
+// stores tile i's products.  The row phase is warp-local: lanes sum their rows of <= 32
+// products, rows with longer segments are reduced by the whole warp (ballot loop).
+template <class V, class I, int NT, int C, int RCAP>
+__global__ void __launch_bounds__(NT) csr_tile_kernel(int64_t rows, int64_t nnz, const I *__restrict__ rp,
+                                                      const I *__restrict__ ci, const V *__restrict__ val,
+                                                      const V *__restrict__ b, int64_t ldb, V *x, int64_t ldx,
+                                                      const int64_t *__restrict__ first_row, int64_t ntiles,
+                                                      int64_t *crow, double *cval) {
+    using L = TileLayout<V, I, C, RCAP>;
+    constexpr int PER = C / NT;
+    static_assert(C % NT == 0, "tile size");
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bar[3];
+    __shared__ TileMeta s_meta[3];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t pol = policy_evict_first();
+    const int64_t G = gridDim.x, bid = blockIdx.x;
+    if (tid == 0) {
+        for (int k = 0; k < 3; ++k) mbar_init(&bar[k], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    auto issue = [&](int64_t t, int64_t r0, int64_t r1, int s) {  // thread 0
+        unsigned char *st = smem + s * L::STAGE;
+        V *sv = reinterpret_cast<V *>(st);
+        I *sc = reinterpret_cast<I *>(st + L::OFF_C);
+        I *sr = reinterpret_cast<I *>(st + L::OFF_R);
+        const int64_t k0 = t * C, k1 = k0 + C < nnz ? k0 + C : nnz;
+        int64_t bv0, bc0, br0 = 0;
+        const uint32_t bv = stage_range(val, k0, k1, nnz, sv, bv0);
+        const uint32_t bc = stage_range(ci, k0, k1, nnz, sc, bc0);
+        const bool srp = RCAP > 0 && r1 - r0 <= RCAP;
+        const uint32_t br = srp ? stage_range(rp, r0, r1 + 1, rows + 1, sr, br0) : 0;
+        s_meta[s] = TileMeta{r0, r1, k0 - bv0, k0 - bc0, r0 - br0, srp};
+        mbar_arrive_expect_tx(&bar[s], bv + bc + br);
+        if (bv) bulk_g2s(sv, val + bv0, bv, &bar[s], pol);
+        if (bc) bulk_g2s(sc, ci + bc0, bc, &bar[s], pol);
+        if (br) bulk_g2s(sr, rp + br0, br, &bar[s], pol);
+    };
+    int64_t nr0 = 0, nr1 = 0;  // thread 0: row range of the next tile to issue
+    if (tid == 0 && bid < ntiles) {
+        issue(bid, first_row[bid], first_row[bid + 1], 0);
+        if (bid + G < ntiles) {
+            nr0 = first_row[bid + G];
+            nr1 = first_row[bid + G + 1];
+        }
+    }
+    for (int64_t i = 0;; ++i) {
+        const int64_t t = bid + i * G, tp = t - G;
+        const bool prod = t < ntiles, red = i > 0 && tp < ntiles;
+        if (!prod && !red) break;
+        if (tid == 0 && t + G < ntiles) {  // stage (i+1)%3 last held tile i-2, reduced at i-1
+            issue(t + G, nr0, nr1, (int)((i + 1) % 3));
+            if (t + 2 * G < ntiles) {
+                nr0 = first_row[t + 2 * G];
+                nr1 = first_row[t + 2 * G + 1];
+            }
+        }
+        // ---- gathers of tile t (consumed after the row phase)
+        const int s = (int)(i % 3);
+        V bb[PER];
+        int cnt = 0;
+        V *sv = nullptr;
+        if (prod) {
+            mbar_wait(&bar[s], (uint32_t)((i / 3) & 1));
+            unsigned char *st = smem + s * L::STAGE;
+            const TileMeta m = s_meta[s];
+            sv = reinterpret_cast<V *>(st) + m.dv;
+            const I *sc = reinterpret_cast<const I *>(st + L::OFF_C) + m.dc;
+            const int64_t k0 = t * C;
+            cnt = (int)((k0 + C < nnz ? k0 + C : nnz) - k0);
+#pragma unroll
+            for (int u = 0; u < PER; ++u) {
+                const int j = tid + u * NT;
+                bb[u] = __ldg(b + (int64_t)sc[j < cnt ? j : cnt - 1] * ldb);
+            }
+        }
+        // ---- rows of tile tp (products in stage (i-1)%3)
+        if (red) {
+            const int sp = (int)((i + 2) % 3);
+            unsigned char *st = smem + sp * L::STAGE;
+            const TileMeta m = s_meta[sp];
+            const V *pv = reinterpret_cast<const V *>(st) + m.dv;
+            const I *sr = reinterpret_cast<const I *>(st + L::OFF_R) + m.dr;  // sr[i - r0] = rp[i]
+            const int64_t r0 = m.r0, r1 = m.r1, k0 = tp * C, k1 = k0 + C < nnz ? k0 + C : nnz;
+            auto rpa = [&](int64_t r) -> int64_t {  // rp[r] for r0 <= r <= r1
+                if (r >= rows) return nnz;
+                return m.staged_rp ? (int64_t)sr[r - r0] : (int64_t)__ldg(rp + r);
+            };
+            auto warp_sum = [&](int kb, int ke) -> double {  // lane-strided partials, fixed tree
+                double acc = 0.0;
+                for (int k = kb + lane; k < ke; k += 32) acc = addd(acc, (double)pv[k]);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc = addd(acc, __shfl_down_sync(0xffffffffu, acc, o));
+                return acc;  // valid in lane 0
+            };
+            if (warp == 0) {  // lead segment (row started before the tile) and empty slots
+                const int64_t lead_end = rpa(r0);
+                if (lead_end > k0) {
+                    const double acc = warp_sum(0, (int)((lead_end < k1 ? lead_end : k1) - k0));
+                    if (lane == 0) {
+                        crow[2 * tp] = r0 - 1;
+                        cval[2 * tp] = acc;
+                    }
+                } else if (lane == 0) {
+                    crow[2 * tp] = -1;
+                }
+                if (lane == 0 && !(r1 > r0 && rpa(r1) > k1)) crow[2 * tp + 1] = -1;
+            }
+            for (int64_t base = r0 + warp * 32; base < r1; base += NT) {
+                const int64_t r = base + lane;
+                int kb = 0, ke = 0;
+                bool cont = false;
+                if (r < r1) {
+                    const int64_t a = rpa(r), e = rpa(r + 1);
+                    kb = (int)(a - k0);
+                    ke = (int)((e < k1 ? e : k1) - k0);
+                    cont = e > k1;
+                    if (ke - kb <= 32) {
+                        double acc = 0.0;
+                        for (int k = kb; k < ke; ++k) acc = addd(acc, (double)pv[k]);
+                        if (!cont) {
+                            x[r * ldx] = (V)acc;
+                        } else {  // the tile's last row continues: trail record
+                            crow[2 * tp + 1] = r;
+                            cval[2 * tp + 1] = acc;
+                        }
+                    }
+                }
+                unsigned lm = __ballot_sync(0xffffffffu, r < r1 && ke - kb > 32);
+                while (lm) {
+                    const int j = __ffs(lm) - 1;
+                    lm &= lm - 1;
+                    const int jb = __shfl_sync(0xffffffffu, kb, j), je = __shfl_sync(0xffffffffu, ke, j);
+                    const bool jc = __shfl_sync(0xffffffffu, cont, j);
+                    const double acc = warp_sum(jb, je);
+                    if (lane == 0) {
+                        if (!jc) {
+                            x[(base + j) * ldx] = (V)acc;
+                        } else {
+                            crow[2 * tp + 1] = base + j;
+                            cval[2 * tp + 1] = acc;
+                        }
+                    }
+                }
+            }
+        }
+        // ---- products of tile t, in place
+        if (prod) {
+#pragma unroll
+            for (int u = 0; u < PER; ++u) {
+                const int j = tid + u * NT;
+                if (j < cnt) sv[j] = (V)mulp(sv[j], bb[u]);
+            }
+        }
+        __syncthreads();  // tile t's products complete; stage (i-1)%3 free for reissue
+    }
+}
+
+// Two-stage variant (no row/product overlap, three block barriers per tile, smaller
+// shared footprint -> one more CTA per SM).  Measured faster for fp64 (config #3: 404
+// vs 497 us), slower for fp32 (556 vs 416 us): launch_csr_tile picks per value type.
+struct TileJob {
+    int32_t rel;     // owned-row index relative to first_row[t], or -1 for the lead segment
+    int32_t kb, ke;  // product range in the tile
+};
+
+template <class V, class I, int NT, int C, int RCAP>
+__global__ void __launch_bounds__(NT) csr_tile2_kernel(int64_t rows, int64_t nnz, const I *__restrict__ rp,
+                                                       const I *__restrict__ ci, const V *__restrict__ val,
+                                                       const V *__restrict__ b, int64_t ldb, V *x, int64_t ldx,
+                                                       const int64_t *__restrict__ first_row, int64_t ntiles,
+                                                       int64_t *crow, double *cval) {
+    using L = TileLayout<V, I, C, RCAP>;
+    constexpr int MAXJ = C / 33 + 4;
+    constexpr int PER = C / NT;
+    static_assert(C % NT == 0, "tile size");
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ TileMeta s_meta[2];
+    __shared__ TileJob s_jobs[MAXJ];
+    __shared__ int s_njobs;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t pol = policy_evict_first();
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    auto issue = [&](int64_t t, int64_t r0, int64_t r1, int s) {  // thread 0
+        unsigned char *st = smem + s * L::STAGE;
+        V *sv = reinterpret_cast<V *>(st);
+        I *sc = reinterpret_cast<I *>(st + L::OFF_C);
+        I *sr = reinterpret_cast<I *>(st + L::OFF_R);
+        const int64_t k0 = t * C, k1 = k0 + C < nnz ? k0 + C : nnz;
+        int64_t bv0, bc0, br0 = 0;
+        const uint32_t bv = stage_range(val, k0, k1, nnz, sv, bv0);
+        const uint32_t bc = stage_range(ci, k0, k1, nnz, sc, bc0);
+        const bool srp = RCAP > 0 && r1 - r0 <= RCAP;
+        const uint32_t br = srp ? stage_range(rp, r0, r1 + 1, rows + 1, sr, br0) : 0;
+        s_meta[s] = TileMeta{r0, r1, k0 - bv0, k0 - bc0, r0 - br0, srp};
+        mbar_arrive_expect_tx(&bar[s], bv + bc + br);
+        if (bv) bulk_g2s(sv, val + bv0, bv, &bar[s], pol);
+        if (bc) bulk_g2s(sc, ci + bc0, bc, &bar[s], pol);
+        if (br) bulk_g2s(sr, rp + br0, br, &bar[s], pol);
+    };
+    int64_t t = blockIdx.x;
+    int64_t nr0 = 0, nr1 = 0;
+    if (tid == 0 && t < ntiles) {
+        issue(t, first_row[t], first_row[t + 1], 0);
+        if (t + gridDim.x < ntiles) {
+            nr0 = first_row[t + gridDim.x];
+            nr1 = first_row[t + gridDim.x + 1];
+        }
+    }
+    for (int it = 0; t < ntiles; t += gridDim.x, ++it) {
+        const int s = it & 1;
+        if (tid == 0) {
+            s_njobs = 0;
+            const int64_t tn = t + gridDim.x;
+            if (tn < ntiles) {
+                issue(tn, nr0, nr1, s ^ 1);
+                if (tn + gridDim.x < ntiles) {
+                    nr0 = first_row[tn + gridDim.x];
+                    nr1 = first_row[tn + gridDim.x + 1];
+                }
+            }
+        }
+        mbar_wait(&bar[s], (it >> 1) & 1);
+        unsigned char *st = smem + s * L::STAGE;
+        const TileMeta m = s_meta[s];
+        V *sv = reinterpret_cast<V *>(st) + m.dv;
+        const I *sc = reinterpret_cast<const I *>(st + L::OFF_C) + m.dc;
+        const I *sr = reinterpret_cast<const I *>(st + L::OFF_R) + m.dr;
+        const int64_t k0 = t * C, k1 = k0 + C < nnz ? k0 + C : nnz;
+        const int cnt = (int)(k1 - k0);
+        {
+            V bb[PER];
+#pragma unroll
+            for (int u = 0; u < PER; ++u) {
+                const int j = tid + u * NT;
+                bb[u] = __ldg(b + (int64_t)sc[j < cnt ? j : cnt - 1] * ldb);
+            }
+#pragma unroll
+            for (int u = 0; u < PER; ++u) {
+                const int j = tid + u * NT;
+                if (j < cnt) sv[j] = (V)mulp(sv[j], bb[u]);
+            }
+        }
+        __syncthreads();
+        const int64_t r0 = m.r0, r1 = m.r1;
+        auto rpa = [&](int64_t i) -> int64_t {
+            if (i >= rows) return nnz;
+            return m.staged_rp ? (int64_t)sr[i - r0] : (int64_t)__ldg(rp + i);
+        };
+        const int64_t lead_end = rpa(r0);
+        const bool has_lead = lead_end > k0;
+        if (tid == 0 && has_lead) {
+            const int e = (int)((lead_end < k1 ? lead_end : k1) - k0);
+            s_jobs[atomicAdd(&s_njobs, 1)] = TileJob{-1, 0, e};
+        }
+        for (int64_t i = r0 + tid; i < r1; i += NT) {
+            const int64_t a = rpa(i), e = rpa(i + 1);
+            const int kb = (int)(a - k0), ke = (int)((e < k1 ? e : k1) - k0);
+            if (ke - kb > 32) {
+                s_jobs[atomicAdd(&s_njobs, 1)] = TileJob{(int)(i - r0), kb, ke};
+            } else {
+                double acc = 0.0;
+                for (int k = kb; k < ke; ++k) acc = addd(acc, (double)sv[k]);
+                if (e <= k1) {
+                    x[i * ldx] = (V)acc;
+                } else {
+                    crow[2 * t + 1] = i;
+                    cval[2 * t + 1] = acc;
+                }
+            }
+        }
+        __syncthreads();
+        const int nj = s_njobs;
+        for (int q = warp; q < nj; q += NT / 32) {
+            const TileJob J = s_jobs[q];
+            double acc = 0.0;
+            for (int k = J.kb + lane; k < J.ke; k += 32) acc = addd(acc, (double)sv[k]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc = addd(acc, __shfl_down_sync(0xffffffffu, acc, o));
+            if (lane == 0) {
+                if (J.rel < 0) {
+                    crow[2 * t] = r0 - 1;
+                    cval[2 * t] = acc;
+                } else {
+                    const int64_t i = r0 + J.rel;
+                    if (k0 + J.ke < rpa(i + 1)) {
+                        crow[2 * t + 1] = i;
+                        cval[2 * t + 1] = acc;
+                    } else {
+                        x[i * ldx] = (V)acc;
+                    }
+                }
+            }
+        }
+        if (tid == 0) {
+            if (!has_lead) crow[2 * t] = -1;
+            if (!(r1 > r0 && rpa(r1) > k1)) crow[2 * t + 1] = -1;
+        }
+        __syncthreads();
+    }
+}
+
+// first_row[t] = first row starting at or after nonzero t*C (rows for t*C beyond every
+// row start)
+template <class I>
+__global__ void tile_partition_kernel(int64_t rows, const I *__restrict__ rp, int64_t C, int64_t ntiles,
+                                      int64_t *first_row) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t > ntiles) return;
+    if (t == ntiles) {  // trailing empty rows (start == nnz) belong to the last tile
+        first_row[t] = rows;
+        return;
+    }
+    const int64_t key = t * C;
+    int64_t lo = 0, hi = rows;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)rp[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    first_row[t] = lo;
+}
+
+// Records in nnz order: [lead_0, trail_0, lead_1, trail_1, ...].  A row crossing tiles
+// a..b has trail_a, lead_{a+1}, ..., lead_b with only empty trail slots between them; the
+// first record of each run sums the run in order and writes the row.
+template <class V>
+__global__ void tile_carry_fixup_kernel(int64_t nrec, const int64_t *crow, const double *cval, V *x,
+                                        int64_t ldx) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= nrec) return;
+    const int64_t r = crow[k];
+    if (r < 0) return;
+    if (k > 0 && (crow[k - 1] == r || (crow[k - 1] < 0 && k > 1 && crow[k - 2] == r))) return;
+    double s = cval[k];
+    for (int64_t u = k + 1; u < nrec; ++u) {
+        if (crow[u] == r) s = addd(s, cval[u]);
+        else if (crow[u] < 0 && (u & 1) && u + 1 < nrec && crow[u + 1] == r) continue;
+        else break;
+    }
+    x[r * ldx] = (V)s;
+}
+
 // Deterministic carry fix-up: runs of equal carry rows are summed in tile order and
 // added once to the row's value (written by the tile that finished the row).
 template <class V>
@@ -706,8 +1087,12 @@ __device__ __forceinline__ void padded_rows(const Epi &epi, const V *__restrict_
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
-            for (int r = 0; r < RPT; ++r)  // padding gathers column 0 and is masked below
-                gg[u][r] = gather_b(epi, b, (int64_t)(cc[u][r] >= 0 ? cc[u][r] : 0) * ldb);
+            for (int r = 0; r < RPT; ++r) {
+                if constexpr (epi_has_gather<Epi>::value)  // branch-free: padding gathers col 0
+                    gg[u][r] = gather_b(epi, b, (int64_t)(cc[u][r] >= 0 ? cc[u][r] : 0) * ldb);
+                else  // predicated plain loads: heavily padded slices issue no pad gathers
+                    gg[u][r] = cc[u][r] >= 0 ? __ldg(b + (int64_t)cc[u][r] * ldb) : (V)0;
+            }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -874,7 +1259,10 @@ __global__ void __launch_bounds__(128) sellp_stream_kernel(int64_t rows, int64_t
                     const int64_t e = o + (int64_t)(k + u) * S;
                     vv[u] = sv[dv + e];
                     cc[u] = sc[dc + e];
-                    bb[u] = gather_b(epi, b, (int64_t)(cc[u] >= 0 ? cc[u] : 0) * ldb);  // padding: masked below
+                    if constexpr (epi_has_gather<Epi>::value)  // padding: col 0, masked below
+                        bb[u] = gather_b(epi, b, (int64_t)(cc[u] >= 0 ? cc[u] : 0) * ldb);
+                    else
+                        bb[u] = cc[u] >= 0 ? __ldg(b + (int64_t)cc[u] * ldb) : (V)0;
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u)

@@ -3,6 +3,8 @@
 #pragma once
 
 #include "../../include/sparseb200.h"
+#include <cstdlib>
+
 #include "spmv.cuh"
 
 namespace sb {
@@ -22,6 +24,16 @@ int persistent_grid(K kernel, int threads, size_t smem) {
 }
 
 constexpr int kMergeNT = 128, kMergeIPT = 8;      // 1024 merge items per tile
+// nnz-tile CSR: nonzeros per tile (1024 / 2048 / 4096 instantiated; 128 / 256 / 256
+// threads), row pointers staged per tile = tile / 2
+inline int tile_nnz_default() {
+    static const int c = [] {
+        const char *e = getenv("SPARSEB200_TILE_C");
+        const int v = e ? atoi(e) : 2048;
+        return (v == 1024 || v == 4096) ? v : 2048;
+    }();
+    return c;
+}
 constexpr int kCooNT = 128, kCooIPT = 8;          // 1024 entries per tile
 constexpr int kElemThreads = 256;
 
@@ -113,6 +125,51 @@ cudaError_t launch_csr_merge(const sb_csr &A, const V *b, int64_t ldb, V *x, int
                            (const double *)P.carry_vals, x, ldx, st);
 }
 
+template <class V, class I, int NT, int C, int RCAP, int STAGES>
+cudaError_t launch_csr_tile_t(const sb_csr &A, const V *b, int64_t ldb, V *x, int64_t ldx, cudaStream_t st) {
+    const sb_csr_plan &P = *A.plan;
+    const int64_t ntiles = P.num_tiles / 2;
+    constexpr size_t smem = STAGES * TileLayout<V, I, C, RCAP>::STAGE;
+    auto kern = STAGES == 3 ? csr_tile_kernel<V, I, NT, C, RCAP> : csr_tile2_kernel<V, I, NT, C, RCAP>;
+    static int configured = 0;
+    if (!configured) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        configured = 1;
+    }
+    int grid = persistent_grid(kern, NT, smem);
+    if (grid > ntiles) grid = (int)ntiles;
+    if (grid < 1) return cudaSuccess;
+    kern<<<grid, NT, smem, st>>>(A.rows, A.nnz, (const I *)A.row_ptrs, (const I *)A.col_idxs,
+                                 (const V *)A.values, b, ldb, x, ldx, (const int64_t *)P.tile_rows, ntiles,
+                                 (int64_t *)P.carry_rows, (double *)P.carry_vals);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    tile_carry_fixup_kernel<V><<<(int)ceil_div(P.num_tiles, 256), 256, 0, st>>>(
+        P.num_tiles, (const int64_t *)P.carry_rows, (const double *)P.carry_vals, x, ldx);
+    return cudaGetLastError();
+}
+
+// Tile shape per value type, measured on config #3 (tools/tile_ab.py, us per SpMV):
+// fp64 two-stage 2048 404 / pipelined 2048 497 / merge-path 561; fp32 pipelined 2048 416 /
+// two-stage 2048 556 / merge-path 452.  SPARSEB200_TILE_C (1024 / 2048 / 4096) and
+// SPARSEB200_TILE_STAGES (2 / 3) override for experiments.
+template <class V, class I>
+cudaError_t launch_csr_tile(const sb_csr &A, const V *b, int64_t ldb, V *x, int64_t ldx, cudaStream_t st) {
+    static const int stages = [] {
+        const char *e = getenv("SPARSEB200_TILE_STAGES");
+        return e ? atoi(e) : (sizeof(V) == 8 ? 2 : 3);
+    }();
+    const int64_t C = A.plan->items_per_tile;
+    if (stages == 2) {
+        if (C == 1024) return launch_csr_tile_t<V, I, 128, 1024, 512, 2>(A, b, ldb, x, ldx, st);
+        if (C == 4096) return launch_csr_tile_t<V, I, 256, 4096, 2048, 2>(A, b, ldb, x, ldx, st);
+        return launch_csr_tile_t<V, I, 256, 2048, 1024, 2>(A, b, ldb, x, ldx, st);
+    }
+    if (C == 1024) return launch_csr_tile_t<V, I, 128, 1024, 512, 3>(A, b, ldb, x, ldx, st);
+    if (C == 4096) return launch_csr_tile_t<V, I, 256, 4096, 2048, 3>(A, b, ldb, x, ldx, st);
+    return launch_csr_tile_t<V, I, 256, 2048, 1024, 3>(A, b, ldb, x, ldx, st);
+}
+
 template <class V>
 __global__ void fill_kernel(int64_t rows, int64_t cols, V *x, int64_t ldx, V v) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rows * cols;
@@ -160,9 +217,11 @@ cudaError_t csr_apply(const sb_csr &A, const V *b, int64_t ldb, V *x_out, int64_
         default: return launch_csr_vector<V, I, 32>(A, b, ldb, epi, st);
         }
     }
-    if (kernel == SB_CSR_MERGE) {
+    if (kernel == SB_CSR_MERGE || kernel == SB_CSR_TILE) {
         if constexpr (epi_has_gather<Epi>::value) return cudaErrorNotSupported;
-        cudaError_t e = launch_csr_merge<V, I>(A, b, ldb, x_out, ldx, st);
+        cudaError_t e = kernel == SB_CSR_MERGE ? launch_csr_merge<V, I>(A, b, ldb, x_out, ldx, st)
+                        : A.nnz == 0            ? launch_fill<V>(A.rows, 1, x_out, ldx, (V)0, st)
+                                                : launch_csr_tile<V, I>(A, b, ldb, x_out, ldx, st);
         if (e != cudaSuccess || is_plain_store<Epi>::value) return e;
         return launch_epilogue_pass<V, I>(A.rows, x_out, ldx, epi, st);
     }
@@ -333,7 +392,7 @@ inline bool matrix_row_owning(const sb_matrix &M) {
     switch (M.format) {
     case SB_FMT_CSR: {
         const sb_csr &A = *(const sb_csr *)M.mat;
-        return !A.plan || A.plan->kernel != SB_CSR_MERGE;
+        return !A.plan || (A.plan->kernel != SB_CSR_MERGE && A.plan->kernel != SB_CSR_TILE);
     }
     case SB_FMT_ELL:
     case SB_FMT_SELLP: return true;

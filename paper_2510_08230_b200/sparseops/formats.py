@@ -171,8 +171,8 @@ class CooMatrix(_SparseBase):
 class CsrMatrix(_SparseBase):
     """Compressed sparse row storage; ``row_ptrs`` has rows + 1 entries.
 
-    ``kernel``: "auto" (row-statistics choice), "stream", "vector", "merge" or
-    "strict" (thread-per-row device replica of the reference loop).
+    ``kernel``: "auto" (row-statistics choice), "stream", "vector", "tile" (fixed-nnz
+    tiles), "merge" or "strict" (thread-per-row device replica of the reference loop).
     """
 
     _fmt, _fmt_id = "csr", _lib.FMT_CSR

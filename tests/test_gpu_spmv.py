@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 
 TYPES = [("float64", "int32"), ("float64", "int64"), ("float32", "int32"), ("float32", "int64")]
 EXACT_KERNELS = ["strict", "stream"]
-TOL_KERNELS = ["vector", "merge", "auto"]
+TOL_KERNELS = ["vector", "merge", "tile", "auto"]
 
 
 @pytest.mark.parametrize("vdt,idt", TYPES)
@@ -88,7 +88,7 @@ def test_known_answers(dev):
     # empty row writes 0 over a NaN pre-fill, for every kernel and format
     dense = np.array([[1.0, 0.0], [0.0, 0.0], [0.0, 2.0]])
     base = sp.csr_from_dense(dev, dense)
-    for kernel in ("strict", "stream", "vector", "merge"):
+    for kernel in ("strict", "stream", "vector", "merge", "tile"):
         x = out(dev, 3, np.float64)
         base.with_kernel(kernel).apply(vec(dev, [1.0, 1.0]), x)
         np.testing.assert_array_equal(host(x), [1.0, 0.0, 2.0], err_msg=kernel)
@@ -142,7 +142,7 @@ def test_linearity_and_determinism(dev):
     rp, ci, v = fixtures.stencil_csr(20, dim=3)
     rng = np.random.default_rng(9)
     b1, b2 = rng.standard_normal(rp.size - 1), rng.standard_normal(rp.size - 1)
-    for kernel in ("stream", "vector", "merge"):
+    for kernel in ("stream", "vector", "merge", "tile"):
         a = csr(dev, rp, ci, v, kernel=kernel)
         runs = []
         for _ in range(3):
@@ -158,8 +158,8 @@ def test_linearity_and_determinism(dev):
 
 
 def test_heavy_rows_merge_and_coo(dev):
-    """Rows far longer than a tile (merge path carries across many tiles; COO runs
-    across tiles) -- the test_linop.py:108-122 heavy-row case at device scale."""
+    """Rows far longer than a tile (nnz-tile and merge-path carries across many tiles; COO
+    runs across tiles) -- the test_linop.py:108-122 heavy-row case at device scale."""
     rng = np.random.default_rng(12)
     n = 3000
     lens = np.ones(n, np.int64)
@@ -171,9 +171,9 @@ def test_heavy_rows_merge_and_coo(dev):
     bv = rng.standard_normal(n)
     ref = sbref.csr_spmv(rp, ci, v, bv)
     a = csr(dev, rp, ci, v)
-    assert a.kernel == "merge"
-    for mat in (a, a.with_kernel("vector"), sp.coo_from_csr(a), sp.hybrid_from_csr(a),
-                sp.sellp_from_csr(a)):
+    assert a.kernel == "tile"
+    for mat in (a, a.with_kernel("merge"), a.with_kernel("vector"), sp.coo_from_csr(a),
+                sp.hybrid_from_csr(a), sp.sellp_from_csr(a)):
         x = out(dev, n, np.float64)
         mat.apply(vec(dev, bv), x)
         assert_close(host(x), ref, rp, v, bv)
@@ -203,8 +203,9 @@ def test_baseline_poisson_bitwise(dev, p, dim):
 
 @pytest.mark.slow
 def test_powerlaw_config3_formats(dev):
-    """Config #3 (4M rows, power-law) at full size, fp64 and fp32: CSR(auto = merge),
-    COO, SELL-P and Hybrid against the oracle's CSR SpMV; ELL is infeasible (560 GB)."""
+    """Config #3 (4M rows, power-law) at full size, fp64 and fp32: CSR (auto = nnz tiles,
+    and merge-path), COO, SELL-P and Hybrid against the oracle's CSR SpMV; ELL is
+    infeasible (560 GB)."""
     n, rows, cols, vals = fixtures.powerlaw_triplets()
     for vdt in (np.float64, np.float32):
         a = gen.powerlaw_csr(dev, precision=sp.Precision.from_dtype(vdt))
@@ -212,8 +213,43 @@ def test_powerlaw_config3_formats(dev):
         rp, ci, v = (t.cpu().numpy() for t in (a.row_ptrs, a.col_idxs, a.values))
         bv = np.random.default_rng(0).random(n).astype(vdt)
         ref = sbref.csr_spmv(rp, ci, v, bv, threads=8)
-        for mat in (a, sp.coo_from_csr(a), sp.sellp_from_csr(a), sp.hybrid_from_csr(a)):
+        assert a.kernel == "tile"
+        for mat in (a, a.with_kernel("merge"), sp.coo_from_csr(a), sp.sellp_from_csr(a),
+                    sp.hybrid_from_csr(a)):
             x = out(dev, n, vdt)
             mat.apply(vec(dev, bv), x)
             assert_close(host(x), ref, rp, v, bv)
             del mat
+
+
+@pytest.mark.parametrize("vdt", [np.float64, np.float32])  # two-stage / pipelined variants
+def test_tile_kernel_edge_cases(dev, vdt):
+    """nnz-tile CSR: rows ending exactly on tile boundaries, rows spanning several whole
+    tiles, runs of empty rows inside and after the last tile (nnz a multiple of the tile),
+    long segments reduced by warps; short rows wholly inside a tile are bit-exact."""
+    rng = np.random.default_rng(21)
+    C = 2048
+    cases = {
+        "boundaries": [C, C, 1, C - 1, 3 * C, 0, 0, 5, C + 7, 0],
+        "multiple": [C] * 4 + [0] * 9,                      # nnz = 4C, trailing empty rows
+        "spanning": [1] * 100 + [5 * C + 3] + [2] * 700 + [0] * 50 + [40] * 90,
+        "short": list(rng.integers(0, 33, 5000)),
+    }
+    for name, lens in cases.items():
+        lens = np.asarray(lens, np.int64)
+        n = lens.size
+        rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+        ci = rng.integers(0, n, int(rp[-1])).astype(np.int32)
+        ci = np.concatenate([np.sort(ci[rp[i]:rp[i + 1]]) for i in range(n)]).astype(np.int32) \
+            if rp[-1] else ci
+        v = rng.standard_normal(int(rp[-1])).astype(vdt)
+        bv = rng.standard_normal(n).astype(vdt)
+        ref = sbref.csr_spmv(rp, ci, v, bv)
+        a = csr(dev, rp, ci, v, n, kernel="tile")
+        x = out(dev, n, vdt)
+        a.apply(vec(dev, bv), x)
+        got = host(x)
+        assert_close(got, ref, rp, v, bv)
+        # rows of <= 32 entries that do not cross a tile boundary keep the sequential order
+        inside = (lens <= 32) & (rp[:-1] // C == np.maximum(rp[1:] - 1, rp[:-1]) // C)
+        np.testing.assert_array_equal(got[inside], ref[inside], err_msg=name)

@@ -49,6 +49,8 @@ def test_plan_selection_host_logic():
     p = select(2_097_152, 14_581_760, 4, 7, [224, 448, 896, 1792])  # Poisson 128^3
     assert p.kernel == _lib.CSR_STREAM and p.block_rows == 128 and p.nnz_cap == 896
     p = select(4_000_000, 63_958_208, 1, 11668, [20000, 20000, 20000, 20000])  # power-law
+    assert p.kernel == _lib.CSR_TILE and p.num_tiles == 2 * -(-63_958_208 // 2048)
+    p = select(4_000_000, 63_958_208, 1, 11668, [20000, 20000, 20000, 20000], force=_lib.CSR_MERGE)
     assert p.kernel == _lib.CSR_MERGE and p.num_tiles == -(-(4_000_000 + 63_958_208) // 1024)
     p = select(10000, 640000, 60, 70, [2240, 4480, 8960, 17920])  # long regular rows
     assert p.kernel == _lib.CSR_VECTOR and p.block_rows == 32

@@ -4,8 +4,8 @@
 
 #1  CSR SpMV fp64, 2-D Poisson 1000^2 (80 MB: fits the 126 MB L2, so every timed launch
     is preceded by a 256 MB L2-flush write, outside the timed events)
-#3  SpMV format sweep on the 4M-row power-law matrix (fp64 and fp32): CSR (plan: merge
-    path), COO, SELL-P(64), Hybrid(q0.8); ELL is infeasible (560 GB) and reported as such.
+#3  SpMV format sweep on the 4M-row power-law matrix (fp64 and fp32): CSR (plan: nnz
+    tiles; merge path beside it), COO, SELL-P(64), Hybrid(q0.8); ELL is infeasible (560 GB) and reported as such.
     GB/s on each format's own bytes and "useful" GB/s on the CSR bytes
 #4  GMRES(30) and BiCGSTAB with Jacobi, fp64 3-D convection-diffusion 256^3, rtol 1e-8
 CPU baselines: the oracle port (oracle/sbref.cpp) on 1 and all host threads.
@@ -128,7 +128,8 @@ def config3(dev, out, args, threads, flush):
         bv = np.random.default_rng(0).random(a.rows).astype(vdt)
         b = sp.dense_from_array(dev, torch.tensor(bv))
         x = sp.dense_create(dev, a.rows, 1, prec, 0.0)
-        mats = {"csr": a, "csr_vector": a.with_kernel("vector"), "coo": sp.coo_from_csr(a),
+        mats = {"csr": a, "csr_merge": a.with_kernel("merge"), "csr_vector": a.with_kernel("vector"),
+                "coo": sp.coo_from_csr(a),
                 "sellp64": sp.sellp_from_csr(a, 64), "hybrid": sp.hybrid_from_csr(a)}
         res = {}
         for name, m in mats.items():
