@@ -594,6 +594,117 @@ int64_t coo_canonicalize(int64_t m, const int64_t *ri, const int64_t *ci, const 
     return nnz;
 }
 
+// ---------------------------------------------------------------- triangular solves
+// _kernels.solve_lower / solve_upper (_kernels.py:91-137): acc = b[i] + 0.0 in fp64;
+// acc -= values[k] * x[j] (product in the value dtype, like numba float32 * float32);
+// x[i] = acc (unit) or acc / diag in fp64, cast on store.  Returns status 0 ok, 1 entry
+// on the wrong side of the diagonal (row), 2 missing / zero diagonal (row).
+template <class V, class I>
+int trsv(int64_t n, const I *rp, const I *ci, const V *val, const V *b, V *x, bool lower, bool unit,
+         int64_t *row) {
+    for (int64_t t = 0; t < n; ++t) {
+        const int64_t i = lower ? t : n - 1 - t;
+        double acc = (double)b[i] + 0.0;
+        double diag = 0.0;
+        bool has_diag = false;
+        for (int64_t k = rp[i]; k < (int64_t)rp[i + 1]; ++k) {
+            const int64_t j = ci[k];
+            if (lower ? j < i : j > i) {
+                acc -= mul(val[k], x[j]);
+            } else if (j == i) {
+                diag = (double)val[k];
+                has_diag = true;
+            } else {
+                *row = i;
+                return 1;
+            }
+        }
+        if (lower && unit) {
+            x[i] = (V)acc;
+        } else {
+            if (!has_diag || diag == 0.0) {
+                *row = i;
+                return 2;
+            }
+            x[i] = (V)(acc / diag);
+        }
+    }
+    *row = -1;
+    return 0;
+}
+
+// ilu0_factorize (precond.py:155-187): IKJ elimination on the stored pattern, in place on
+// a copy of the values, arithmetic in the value dtype.  Returns -1 or the zero-pivot row.
+template <class V, class I>
+int64_t ilu0(int64_t n, const I *rp, const I *ci, V *vals) {
+    std::vector<int64_t> dpos(n, -1);
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t k = rp[i]; k < (int64_t)rp[i + 1]; ++k)
+            if ((int64_t)ci[k] == i) dpos[i] = k;
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t s = rp[i], e = rp[i + 1];
+        for (int64_t idx = s; idx < e; ++idx) {
+            const int64_t k = ci[idx];
+            if (k >= i) break;
+            const int64_t dk = dpos[k];
+            const V ukk = dk >= 0 ? vals[dk] : (V)0;
+            if (ukk == (V)0) return k;
+            const V lik = vals[idx] / ukk;
+            vals[idx] = lik;
+            for (int64_t idx2 = dk + 1; idx2 < (int64_t)rp[k + 1]; ++idx2) {
+                const I j = ci[idx2];
+                const I *pos = std::lower_bound(ci + s, ci + e, j);
+                if (pos != ci + e && *pos == j) {
+                    V &a = vals[pos - ci];
+                    a = a - lik * vals[idx2];
+                }
+            }
+        }
+        if (dpos[i] < 0 || vals[dpos[i]] == (V)0) return i;
+    }
+    return -1;
+}
+
+// ic0_factorize (precond.py:205-256) on the lower pattern (cols <= i, diagonal last):
+// Python-float (fp64) arithmetic throughout, cast to the value dtype at the end.
+// Returns -1 or the row of the first non-positive / missing pivot.
+template <class V, class I>
+int64_t ic0(int64_t n, const I *lp, const I *lc, const V *a_lower, V *out) {
+    std::vector<double> lv((size_t)lp[n], 0.0);
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t si = lp[i], ei = lp[i + 1];
+        for (int64_t pos = si; pos < ei; ++pos) {
+            const int64_t j = lc[pos];
+            double s = (double)a_lower[pos];
+            const int64_t sj = lp[j], ej = lp[j + 1];
+            int64_t pi = si, pj = sj;
+            while (pi < ei && pj < ej) {
+                const int64_t c1 = lc[pi], c2 = lc[pj];
+                if (c1 >= j || c2 >= j) break;
+                if (c1 == c2) {
+                    s -= lv[pi] * lv[pj];
+                    ++pi;
+                    ++pj;
+                } else if (c1 < c2) {
+                    ++pi;
+                } else {
+                    ++pj;
+                }
+            }
+            if (j == i) {
+                if (s <= 0.0) return i;
+                lv[pos] = std::sqrt(s);
+            } else {
+                if (ej == sj || (int64_t)lc[ej - 1] != j || lv[ej - 1] == 0.0) return j;
+                lv[pos] = s / lv[ej - 1];
+            }
+        }
+        if (ei == si || (int64_t)lc[ei - 1] != i) return i;
+    }
+    for (int64_t k = 0; k < (int64_t)lp[n]; ++k) out[k] = (V)lv[k];
+    return -1;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- exported C ABI (ctypes)
@@ -645,6 +756,17 @@ int64_t coo_canonicalize(int64_t m, const int64_t *ri, const int64_t *ci, const 
     extern "C" void ref_sellp_spmv_##VN##_##IN(int64_t rows, int64_t S, const I *sl, const I *ss,  \
                                                const I *sc, const V *sv, const V *b, V *x) {       \
         sellp_spmv(rows, S, sl, ss, sc, sv, b, x);                                                 \
+    }                                                                                              \
+    extern "C" int ref_trsv_##VN##_##IN(int64_t n, const I *rp, const I *ci, const V *val,         \
+                                        const V *b, V *x, int lower, int unit, int64_t *row) {     \
+        return trsv(n, rp, ci, val, b, x, lower != 0, unit != 0, row);                             \
+    }                                                                                              \
+    extern "C" int64_t ref_ilu0_##VN##_##IN(int64_t n, const I *rp, const I *ci, V *vals) {        \
+        return ilu0(n, rp, ci, vals);                                                              \
+    }                                                                                              \
+    extern "C" int64_t ref_ic0_##VN##_##IN(int64_t n, const I *lp, const I *lc, const V *al,       \
+                                           V *out) {                                               \
+        return ic0(n, lp, lc, al, out);                                                            \
     }                                                                                              \
     extern "C" void ref_solve_##VN##_##IN(int kind, int64_t n, const I *rp, const I *ci,           \
                                           const V *val, const V *inv, const V *b, V *x,            \

@@ -62,6 +62,9 @@ def lib():
             getattr(_lib, f"ref_coo_canonicalize_{vn}").restype = ctypes.c_int64
             for ix in ("i32", "i64"):
                 getattr(_lib, f"ref_jacobi_create_{vn}_{ix}").restype = ctypes.c_int64
+                getattr(_lib, f"ref_trsv_{vn}_{ix}").restype = ctypes.c_int
+                getattr(_lib, f"ref_ilu0_{vn}_{ix}").restype = ctypes.c_int64
+                getattr(_lib, f"ref_ic0_{vn}_{ix}").restype = ctypes.c_int64
     return _lib
 
 
@@ -303,3 +306,51 @@ def solve(kind, row_ptrs, col_idxs, values, b, x0=None, inv_diag=None, max_iters
               int(log.status), int(log.status_iteration),
               hist[: min(int(log.history_len), cap)].tolist())
     return out, x
+
+
+# ---------------------------------------------------------------- ILU(0) / IC(0) / SpTRSV
+def trsv(row_ptrs, col_idxs, values, b, lower=True, unit_diag=False):
+    """_kernels.solve_lower / solve_upper: returns (status, row, x) with status 0 ok,
+    1 entry on the wrong side of the diagonal, 2 missing / zero diagonal."""
+    values = np.ascontiguousarray(values)
+    col_idxs = np.ascontiguousarray(col_idxs)
+    row_ptrs = _c(row_ptrs, col_idxs.dtype)
+    n = row_ptrs.size - 1
+    b = _c(b, values.dtype)
+    x = np.zeros(n, values.dtype)
+    row = I64(0)
+    fn = getattr(lib(), f"ref_trsv_{_VN[values.dtype]}_{_IN[col_idxs.dtype]}")
+    st = fn(I64(n), _p(row_ptrs), _p(col_idxs), _p(values), _p(b), _p(x), int(lower), int(unit_diag),
+            ctypes.byref(row))
+    return int(st), int(row.value), x
+
+
+def ilu0(row_ptrs, col_idxs, values):
+    """ilu0_factorize on the stored pattern: (zero_pivot_row or -1, factored values)."""
+    vals = np.array(values, copy=True)
+    col_idxs = np.ascontiguousarray(col_idxs)
+    row_ptrs = _c(row_ptrs, col_idxs.dtype)
+    fn = getattr(lib(), f"ref_ilu0_{_VN[vals.dtype]}_{_IN[col_idxs.dtype]}")
+    return int(fn(I64(row_ptrs.size - 1), _p(row_ptrs), _p(col_idxs), _p(vals))), vals
+
+
+def split_lu(row_ptrs, col_idxs, values, lower_incl_diag=False):
+    """_split_lu (precond.py:190-202): strict lower (or lower incl. diagonal) / the rest."""
+    rp = np.asarray(row_ptrs, np.int64)
+    n = rp.size - 1
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    cols = np.asarray(col_idxs)
+    m = cols <= rows if lower_incl_diag else cols < rows
+    def part(mask):
+        ptr = np.concatenate([[0], np.cumsum(np.bincount(rows[mask], minlength=n))])
+        return ptr.astype(cols.dtype), cols[mask].copy(), np.asarray(values)[mask].copy()
+    return part(m), part(~m)
+
+
+def ic0(row_ptrs, col_idxs, values):
+    """ic0_factorize: (pivot_error_row or -1, (lp, lc, lv)) on the lower pattern of A."""
+    (lp, lc, la), _ = split_lu(row_ptrs, col_idxs, values, lower_incl_diag=True)
+    out = np.zeros_like(la)
+    fn = getattr(lib(), f"ref_ic0_{_VN[la.dtype]}_{_IN[lc.dtype]}")
+    st = int(fn(I64(lp.size - 1), _p(lp), _p(lc), _p(la), _p(out)))
+    return st, (lp, lc, out)

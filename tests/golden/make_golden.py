@@ -184,10 +184,122 @@ def blas1():
     np.savez_compressed(os.path.join(HERE, "blas1.npz"), **out)
 
 
+def factorizations():
+    """ILU(0), IC(0) and the triangular solves (precond.py:155-287, _kernels.py:91-137):
+    factor values, apply outputs and the error rows of the reference, for fp64 and fp32
+    on stencils and random diagonally dominant / SPD matrices; plus ILU-preconditioned
+    GMRES and IC-preconditioned CG runs (the README's Listing 1 pipeline)."""
+    rng = np.random.default_rng(77)
+    mats, meta = [], []
+    cases = []
+    for vdt in (np.float64, np.float32):
+        cases.append(("poisson2d_9", fixtures.poisson2d_triplets(9), vdt, True))
+        cases.append(("convdiff3d_6", fixtures.stencil3d_triplets(6, 0.5), vdt, False))
+        for t in range(3):
+            n = int(rng.integers(20, 90))
+            rows, cols, vals = fixtures.random_sparse_triplets(rng, n, n, 0.08)
+            d = np.arange(n)
+            # diagonally dominant nonsymmetric (ILU) and its symmetric part (IC)
+            rr = np.concatenate([rows, d]); cc = np.concatenate([cols, d])
+            vv = np.concatenate([vals, np.full(n, 0.0)])
+            a0 = ref_csr(n, n, rr, cc, vv, np.float64).to_dense()
+            dense = a0 + np.diag(np.abs(a0).sum(axis=1) + 1.0)
+            r2, c2 = np.nonzero(dense)
+            cases.append((f"rand{t}", (n, r2, c2, dense[r2, c2]), vdt, False))
+            sym = dense + dense.T
+            r3, c3 = np.nonzero(sym)
+            cases.append((f"randspd{t}", (n, r3, c3, sym[r3, c3]), vdt, True))
+    for name, (n, ri, ci, v), vdt, spd in cases:
+        a = ref_csr(n, n, ri, ci, v, vdt)
+        bv = rng.standard_normal(n).astype(vdt)
+        f = sp.ilu0_factorize(a)
+        y = sp.dense_create(REF, n, 1, PREC[vdt], 0.0)
+        sp.ilu_apply(f, vec(bv, vdt), y)
+        rec = dict(row_ptrs=a.row_ptrs, col_idxs=a.col_idxs, values=a.values, b=bv,
+                   ilu_l_ptrs=f.l.row_ptrs, ilu_l_cols=f.l.col_idxs, ilu_l_vals=f.l.values,
+                   ilu_u_ptrs=f.u.row_ptrs, ilu_u_cols=f.u.col_idxs, ilu_u_vals=f.u.values,
+                   ilu_x=y.values.copy())
+        if spd:
+            g = sp.ic0_factorize(a)
+            z = sp.dense_create(REF, n, 1, PREC[vdt], 0.0)
+            sp.ic_apply(g, vec(bv, vdt), z)
+            rec.update(ic_l_ptrs=g.l.row_ptrs, ic_l_cols=g.l.col_idxs, ic_l_vals=g.l.values,
+                       ic_x=z.values.copy())
+        else:
+            for k in ("ic_l_ptrs", "ic_l_cols"):
+                rec[k] = np.zeros(0, a.col_idxs.dtype)
+            rec["ic_l_vals"] = np.zeros(0, vdt)
+            rec["ic_x"] = np.zeros(0, vdt)
+        mats.append({k: np.asarray(v_) for k, v_ in rec.items()})
+        meta.append(dict(name=name, dtype=np.dtype(vdt).name, spd=spd))
+    for vdt in (np.float64, np.float32):
+        sel = [m for m, md in zip(mats, meta) if md["dtype"] == np.dtype(vdt).name]
+        np.savez_compressed(os.path.join(HERE, f"factor_{np.dtype(vdt).name}.npz"), **pack(sel))
+    # error rows: zero pivots, indefinite pivots, wrong-side entries, singular triangles
+    errs = {}
+    def err_row(fn):
+        try:
+            fn()
+        except sp.errors.SparseOpsError as exc:
+            return type(exc).__name__, int(getattr(exc, "row", -1))
+        return None, -1
+    z2 = np.array([[0.0, 1.0], [1.0, 0.0]])
+    errs["ilu_zero_pivot"] = err_row(lambda: sp.ilu0_factorize(sp.csr_from_dense(REF, z2, keep_zeros=True)))
+    late = np.eye(5) * 2.0
+    late[3, 3] = 0.0
+    errs["ilu_zero_pivot_row3"] = err_row(lambda: sp.ilu0_factorize(sp.csr_from_dense(REF, late, keep_zeros=True)))
+    errs["ic_indefinite"] = err_row(lambda: sp.ic0_factorize(sp.csr_from_dense(REF, np.diag([1.0, 4.0, -1.0, 2.0]))))
+    upper = np.triu(np.ones((4, 4)))
+    errs["lower_not_triangular"] = err_row(lambda: sp.solve_lower_tri(
+        sp.csr_from_dense(REF, upper), vec(np.ones(4), np.float64), sp.dense_create(REF, 4, 1, sp.Precision.double, 0.0)))
+    def tri(lower, zero_at):  # triangle of ones with an explicit zero on one diagonal slot
+        t = [(i, j, 0.0 if (i == j == zero_at) else 1.0) for i in range(4) for j in range(4)
+             if (j <= i if lower else j >= i)]
+        return sp.csr_from_coo(sp.coo_from_triplets(REF, 4, 4, t))
+    errs["lower_singular"] = err_row(lambda: sp.solve_lower_tri(
+        tri(True, 2), vec(np.ones(4), np.float64), sp.dense_create(REF, 4, 1, sp.Precision.double, 0.0)))
+    errs["upper_not_triangular"] = err_row(lambda: sp.solve_upper_tri(
+        sp.csr_from_dense(REF, np.tril(np.ones((4, 4)))), vec(np.ones(4), np.float64),
+        sp.dense_create(REF, 4, 1, sp.Precision.double, 0.0)))
+    errs["upper_singular"] = err_row(lambda: sp.solve_upper_tri(
+        tri(False, 1), vec(np.ones(4), np.float64), sp.dense_create(REF, 4, 1, sp.Precision.double, 0.0)))
+    # preconditioned solver runs
+    runs = {}
+    n2, r2, c2, v2 = fixtures.poisson2d_triplets(16)
+    a = ref_csr(n2, n2, r2, c2, v2)
+    for name, cls, pre, crit, kw in (
+            ("gmres30_ilu_poisson2d_16", "Gmres", "ilu", [sp.Iteration(1000), sp.ResidualNorm(1e-6)], {"krylov_dim": 30}),
+            ("gmres10_ilu_convdiff3d_8", "Gmres", "ilu", [sp.Iteration(1000), sp.ResidualNorm(1e-8)], {"krylov_dim": 10}),
+            ("cg_ic_poisson2d_16", "Cg", "ic", [sp.Iteration(1000), sp.ResidualNorm(1e-8)], {}),
+            ("cg_ilu_poisson3d_8", "Cg", "ilu", [sp.Iteration(1000), sp.ResidualNorm(1e-8)], {})):
+        if "convdiff" in name:
+            n, ri, ci, v = fixtures.stencil3d_triplets(8, 0.5)
+            m_ = ref_csr(n, n, ri, ci, v)
+            src = ("stencil3d", 8, 0.5)
+        elif "poisson3d" in name:
+            n, ri, ci, v = fixtures.stencil3d_triplets(8, 0.0)
+            m_ = ref_csr(n, n, ri, ci, v)
+            src = ("stencil3d", 8, 0.0)
+        else:
+            m_, n, src = a, n2, ("poisson2d", 16, 0.0)
+        prec = sp.ilu0_factorize(m_) if pre == "ilu" else sp.ic0_factorize(m_)
+        b = sp.dense_create(REF, n, 1, sp.Precision.double, 1.0)
+        x = sp.dense_create(REF, n, 1, sp.Precision.double, 0.0)
+        log = getattr(sp, cls)(m_, criteria=crit, preconditioner=prec, **kw).solve(b, x)
+        runs[name] = dict(source=list(src), solver=cls.lower(), precond=pre,
+                          max_iters=1000, reduction_factor=crit[1].reduction_factor,
+                          krylov_dim=kw.get("krylov_dim"), iterations=log.iterations,
+                          converged=log.converged, stop_reason=log.stop_reason,
+                          history=list(map(float, log.residual_history)))
+    with open(os.path.join(HERE, "factor.json"), "w") as fh:
+        json.dump({"cases": meta, "errors": errs, "solver_runs": runs}, fh, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
     spmv_suite()
     canonicalization()
     stencils_and_jacobi()
     blas1()
     solver_goldens()
+    factorizations()
     print("golden fixtures written to", HERE)

@@ -6,6 +6,8 @@ outputs must match BIT FOR BIT: the oracle restates the reference's arithmetic
 order exactly, which is what makes it a trustworthy checker for the GPU path.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -129,3 +131,67 @@ def test_ell_sellp_layouts_roundtrip():
         np.testing.assert_array_equal(sbref.ell_spmv(rows, w, stride, ec, ev, b), m["x"])
         sl, ss, sc, sv = sbref.sellp_from_csr(rp, ci, v, 64)
         np.testing.assert_array_equal(sbref.sellp_spmv(rows, 64, sl, ss, sc, sv, b), m["x"])
+
+
+def _transpose(rp, ci, v):
+    n = rp.size - 1
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    order = np.lexsort((rows, ci))
+    tp = np.concatenate([[0], np.cumsum(np.bincount(ci, minlength=n))]).astype(rp.dtype)
+    return tp, rows[order].astype(ci.dtype), v[order]
+
+
+@pytest.mark.parametrize("vdt", ["float64", "float32"])
+def test_oracle_factorizations_match_reference(vdt):
+    """ILU(0) factors + apply, IC(0) factor + apply: the oracle restatement equals the
+    reference's outputs (tests/golden/factor_*.npz) bit for bit."""
+    for m in golden_io.unpack(golden_io.load(f"factor_{vdt}.npz")):
+        rp, ci, v, b = m["row_ptrs"], m["col_idxs"], m["values"], m["b"]
+        st, fv = sbref.ilu0(rp, ci, v)
+        assert st == -1
+        (lp, lc, lv), (up, uc, uv) = sbref.split_lu(rp, ci, fv)
+        for got, want in ((lp, m["ilu_l_ptrs"]), (lc, m["ilu_l_cols"]), (lv, m["ilu_l_vals"]),
+                          (up, m["ilu_u_ptrs"]), (uc, m["ilu_u_cols"]), (uv, m["ilu_u_vals"])):
+            np.testing.assert_array_equal(got, want)
+        s1, _, y = sbref.trsv(lp, lc, lv, b, lower=True, unit_diag=True)
+        s2, _, x = sbref.trsv(up, uc, uv, y, lower=False)
+        assert s1 == s2 == 0
+        np.testing.assert_array_equal(x, m["ilu_x"])
+        if m["ic_l_ptrs"].size:
+            st, (gp, gc, gv) = sbref.ic0(rp, ci, v)
+            assert st == -1
+            np.testing.assert_array_equal(gp, m["ic_l_ptrs"])
+            np.testing.assert_array_equal(gc, m["ic_l_cols"])
+            np.testing.assert_array_equal(gv, m["ic_l_vals"])
+            s1, _, y = sbref.trsv(gp, gc, gv, b, lower=True)
+            tp, tc, tv = _transpose(gp, gc, gv)
+            s2, _, x = sbref.trsv(tp, tc, tv, y, lower=False)
+            assert s1 == s2 == 0
+            np.testing.assert_array_equal(x, m["ic_x"])
+
+
+def test_oracle_factorization_errors_match_reference():
+    import json
+    with open(os.path.join(golden_io.GOLDEN, "factor.json")) as fh:
+        errs = json.load(fh)["errors"]
+    def csr_of(dense, keep=True):
+        r, c = np.nonzero(np.ones_like(dense)) if keep else np.nonzero(dense)
+        return fixtures.canonical_csr(dense.shape[0], r, c, dense[r, c])
+    assert sbref.ilu0(*csr_of(np.array([[0.0, 1.0], [1.0, 0.0]])))[0] == errs["ilu_zero_pivot"][1]
+    late = np.eye(5) * 2.0
+    late[3, 3] = 0.0
+    rr, cc = np.nonzero(np.eye(5))
+    rp, ci, v = fixtures.canonical_csr(5, rr, cc, late[rr, cc])
+    assert sbref.ilu0(rp, ci, v)[0] == errs["ilu_zero_pivot_row3"][1]
+    assert sbref.ic0(*csr_of(np.diag([1.0, 4.0, -1.0, 2.0]), keep=False))[0] == errs["ic_indefinite"][1]
+    up = csr_of(np.triu(np.ones((4, 4))), keep=False)
+    assert sbref.trsv(*up, np.ones(4), lower=True)[:2] == (1, errs["lower_not_triangular"][1])
+    lo = csr_of(np.tril(np.ones((4, 4))), keep=False)
+    assert sbref.trsv(*lo, np.ones(4), lower=False)[:2] == (1, errs["upper_not_triangular"][1])
+    for lower, z, key in ((True, 2, "lower_singular"), (False, 1, "upper_singular")):
+        mask = np.tril(np.ones((4, 4))) if lower else np.triu(np.ones((4, 4)))
+        dense = mask.copy()
+        dense[z, z] = 0.0
+        r, c = np.nonzero(mask)
+        rp, ci, v = fixtures.canonical_csr(4, r, c, dense[r, c])
+        assert sbref.trsv(rp, ci, v, np.ones(4), lower=lower)[:2] == (2, errs[key][1])
