@@ -58,7 +58,11 @@ typedef enum {
     SB_ERR_NUMERIC_FAILURE = 7,    /* NumericFailureError                            errors.py:96 */
     SB_ERR_SINGULAR_DIAGONAL = 8,  /* SingularDiagonalError (row)                    errors.py:115-121 */
     SB_ERR_CUDA = 9,               /* CUDA runtime failure (no reference analogue) */
-    SB_ERR_NCCL = 10               /* NCCL failure (multi-GPU only) */
+    SB_ERR_NCCL = 10,              /* NCCL failure (multi-GPU only) */
+    SB_ERR_ZERO_PIVOT = 11,        /* ZeroPivotError (row)        precond.py:155-187 */
+    SB_ERR_INDEFINITE_PIVOT = 12,  /* IndefinitePivotError (row)  precond.py:205-256 */
+    SB_ERR_NOT_TRIANGULAR = 13,    /* NotTriangularError (row)    linop.py:169-198 */
+    SB_ERR_SINGULAR_TRIANGLE = 14  /* SingularTriangleError (row) linop.py:169-198 */
 } sb_status;
 
 typedef struct {
@@ -364,6 +368,66 @@ SB_DIST_DECLS(float, i32)
 SB_DIST_DECLS(float, i64)
 SB_DIST_DECLS(double, i32)
 SB_DIST_DECLS(double, i64)
+
+/* ---------------------------------------------------------------- ILU(0) / IC(0) + SpTRSV
+   SURVEY.md 8f f4: precond.py:155-287 (ilu0_factorize, _split_lu, ic0_factorize,
+   IluFactors / IcFactor.apply), linop.py:169-198 (solve_lower_tri / solve_upper_tri),
+   _kernels.py:91-137.  Sync-free device sweeps (rows claimed in solve order, per-row ready
+   flags), bit-exact with the reference loops.  Workspace: sb_tri_workspace_bytes(n). */
+size_t sb_tri_workspace_bytes(int64_t n);
+
+/* a two-factor triangular preconditioner x = U^{-1} (L^{-1} b) for the device solvers:
+   ILU(0): l = strict lower (unit diagonal implicit, l_unit = 1), u = upper incl. diagonal;
+   IC(0):  l = L (l_unit = 0), u = L^T */
+typedef struct {
+    const sb_csr *l;
+    int32_t l_unit;
+    int32_t pad;
+    const sb_csr *u;
+    void *workspace; /* sb_tri_workspace_bytes(rows) */
+} sb_tri_precond;
+
+#define SB_TRI_DECLS(VN, IN)                                                                      \
+    /* x = T^{-1} b (lower: forward, upper: backward); NotTriangular / SingularTriangle rows */  \
+    sb_status sb_csr_trisolve_##VN##_##IN(const sb_csr *t, int32_t lower, int32_t unit_diag,     \
+                                          const sb_dense *b, sb_dense *x, void *workspace,       \
+                                          sb_stream_t stream, sb_error *err);                    \
+    sb_status sb_csr_tri_check_##VN##_##IN(const sb_csr *t, int32_t lower, int32_t unit_diag,    \
+                                           void *workspace, sb_stream_t stream, sb_error *err);  \
+    /* ILU(0) values on A's pattern (values_out: nnz); diag_workspace: int64[rows] */            \
+    sb_status sb_ilu0_##VN##_##IN(const sb_csr *a, void *values_out, void *workspace,            \
+                                  void *diag_workspace, sb_stream_t stream, sb_error *err);      \
+    /* IC(0) on the lower pattern (lp, lc, la = A's entries with col <= row); scratch:         \
+       double[nnz of the lower pattern] */                                                      \
+    sb_status sb_ic0_##VN##_##IN(int64_t n, const void *lp, const void *lc, const void *la,      \
+                                 void *values_out, void *workspace, void *scratch,               \
+                                 sb_stream_t stream, sb_error *err);                             \
+    /* _split_lu scatter given the split row pointers (lp, up = row_ptrs - lp) */              \
+    sb_status sb_csr_split_scatter_##VN##_##IN(int64_t n, const void *rp, const void *ci,        \
+                                               const void *val, const void *lp, const void *up,  \
+                                               void *lc, void *lv, void *uc, void *uv,           \
+                                               sb_stream_t stream, sb_error *err);               \
+    /* CG / GMRES with a triangular-factor preconditioner (ILU / IC) */                         \
+    sb_status sb_cg_solve_tri_##VN##_##IN(const sb_matrix *a, const sb_tri_precond *m,           \
+                                          const sb_dense *b, sb_dense *x,                        \
+                                          const sb_criteria *crit, void *workspace, sb_log *log, \
+                                          sb_stream_t stream, sb_error *err);                    \
+    sb_status sb_gmres_solve_tri_##VN##_##IN(const sb_matrix *a, const sb_tri_precond *m,        \
+                                             const sb_dense *b, sb_dense *x,                     \
+                                             const sb_criteria *crit, int64_t krylov_dim,        \
+                                             void *workspace, sb_log *log, sb_stream_t stream,   \
+                                             sb_error *err);
+
+SB_TRI_DECLS(float, i32)
+SB_TRI_DECLS(float, i64)
+SB_TRI_DECLS(double, i32)
+SB_TRI_DECLS(double, i64)
+
+/* per-row counts of entries with col < row (incl_diag: col <= row), for _split_lu */
+sb_status sb_csr_split_count_i32(int64_t n, const void *rp, const void *ci, int32_t incl_diag,
+                                 int64_t *counts, sb_stream_t stream, sb_error *err);
+sb_status sb_csr_split_count_i64(int64_t n, const void *rp, const void *ci, int32_t incl_diag,
+                                 int64_t *counts, sb_stream_t stream, sb_error *err);
 
 /* solver ids for sb_solver_workspace_bytes */
 enum { SB_SOLVER_CG = 0, SB_SOLVER_CGS = 1, SB_SOLVER_GMRES = 2, SB_SOLVER_BICGSTAB = 3 };

@@ -103,6 +103,11 @@ class SbDistPart(ctypes.Structure):
                 ("inv_diag", c_vp), ("b", SbDense), ("x", SbDense), ("workspace", c_vp)]
 
 
+class SbTriPrecond(ctypes.Structure):
+    _fields_ = [("l", ctypes.POINTER(SbCsr)), ("l_unit", c_i32), ("pad", c_i32),
+                ("u", ctypes.POINTER(SbCsr)), ("workspace", c_vp)]
+
+
 FMT_CSR, FMT_COO, FMT_ELL, FMT_SELLP, FMT_HYBRID = 0, 1, 2, 3, 4
 CSR_AUTO, CSR_STRICT, CSR_STREAM, CSR_VECTOR, CSR_MERGE, CSR_TILE = 0, 1, 2, 3, 4, 5
 CSR_KERNELS = {"auto": CSR_AUTO, "strict": CSR_STRICT, "stream": CSR_STREAM,
@@ -146,6 +151,17 @@ _VI_PROTOS = {
                                        c_i64, c_vp, P(SbLog), c_vp, P(SbError)]),
     "sb_dist_cg_solve_{v}_{i}": (c_i32, [P(SbDistPart), c_i32, c_vp, P(SbCriteria), P(SbLog),
                                          c_vp, P(SbError)]),
+    "sb_csr_trisolve_{v}_{i}": (c_i32, [P(SbCsr), c_i32, c_i32, P(SbDense), P(SbDense), c_vp, c_vp,
+                                        P(SbError)]),
+    "sb_csr_tri_check_{v}_{i}": (c_i32, [P(SbCsr), c_i32, c_i32, c_vp, c_vp, P(SbError)]),
+    "sb_ilu0_{v}_{i}": (c_i32, [P(SbCsr), c_vp, c_vp, c_vp, c_vp, P(SbError)]),
+    "sb_ic0_{v}_{i}": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, P(SbError)]),
+    "sb_csr_split_scatter_{v}_{i}": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                             c_vp, c_vp, P(SbError)]),
+    "sb_cg_solve_tri_{v}_{i}": (c_i32, [P(SbMatrix), P(SbTriPrecond), P(SbDense), P(SbDense),
+                                        P(SbCriteria), c_vp, P(SbLog), c_vp, P(SbError)]),
+    "sb_gmres_solve_tri_{v}_{i}": (c_i32, [P(SbMatrix), P(SbTriPrecond), P(SbDense), P(SbDense),
+                                           P(SbCriteria), c_i64, c_vp, P(SbLog), c_vp, P(SbError)]),
 }
 _I_PROTOS = {
     "sb_csr_row_stats_{i}": (c_i32, [c_i64, c_vp, c_vp, P(SbRowStats), c_vp, P(SbError)]),
@@ -158,6 +174,7 @@ _I_PROTOS = {
                                           c_vp, P(SbError)]),
     "sb_stencil_csr_float_{i}": (c_i32, [c_i64, c_i32, c_f64, c_i64, c_i64, c_vp, c_vp, c_vp,
                                          c_vp, P(SbError)]),
+    "sb_csr_split_count_{i}": (c_i32, [c_i64, c_vp, c_vp, c_i32, c_vp, c_vp, P(SbError)]),
 }
 _PLAIN_PROTOS = {
     "sb_version": (c_i32, []),
@@ -165,6 +182,7 @@ _PLAIN_PROTOS = {
     "sb_set_graph_mode": (None, [c_i32]),
     "sb_set_cg_fused": (None, [c_i32]),
     "sb_cg_last_loop": (c_i32, []),
+    "sb_tri_workspace_bytes": (c_sz, [c_i64]),
     "sb_csr_plan_select": (c_i32, [P(SbRowStats), c_i32, c_i32, c_i32, P(SbCsrPlan),
                                    P(SbError)]),
     "sb_coo_tile_entries": (c_i64, []),
@@ -252,6 +270,14 @@ def raise_for(status: int, err: SbError):
         raise E.SingularDiagonalError(int(err.row), msg)
     if status == 10:
         raise E.CommunicationError(msg)
+    if status == 11:
+        raise E.ZeroPivotError(int(err.row), msg)
+    if status == 12:
+        raise E.IndefinitePivotError(int(err.row), msg)
+    if status == 13:
+        raise E.NotTriangularError(int(err.row), msg)
+    if status == 14:
+        raise E.SingularTriangleError(int(err.row), msg)
     raise E.DeviceError(f"{msg} (status {status})")
 
 

@@ -5,6 +5,7 @@
 #include <vector>
 
 #include "solver_common.cuh"
+#include "trisolve.cuh"
 
 namespace sb {
 
@@ -496,8 +497,156 @@ static std::atomic<int> g_cg_mode{[] {
 constexpr size_t kPersistentMaxVectorBytes = 24u << 20;
 static thread_local int g_cg_last_loop = -1;  // loop shape of this thread's last CG solve
 
+// ---------------------------------------------------------------- CG with ILU / IC factors
+// z = U^{-1} (L^{-1} r) between the update and the direction: the update kernel stops at
+// the criteria (r.r), two triangular sweeps form z, a dot kernel forms r.z and beta
+// (solvers.py:207-222 order: x, r, ||r|| check, z = M r, rz_new, beta, p).
+template <class V>
+struct CgInitNoZ : SkipNone {  // r = b - A x0; b.b, r.r (z follows from the sweeps)
+    using value_type = V;
+    const V *b, *t;
+    V *r;
+    template <int W>
+    __device__ __forceinline__ void elem(int64_t i, double (&part)[2]) const {
+        const auto B = ldp<W>(b, i), T = ldp<W>(t, i);
+        Pk<V, W> R;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            R.v[w] = axpy_e(-1.0, T.v[w], B.v[w]);
+            part[0] = addd(part[0], mulp(B.v[w], B.v[w]));
+            part[1] = addd(part[1], mulp(R.v[w], R.v[w]));
+        }
+        stp<W>(r, i, R);
+    }
+    __device__ __forceinline__ void last(Ctl *c, const double (&tot)[2]) const {
+        c->bnorm = sqrt(tot[0]);
+        c->rnorm = sqrt(tot[1]);
+        c->iter = 0;
+        if (c->rnorm == 0.0) exact_log(c);
+    }
+};
+
+template <class V, bool INIT>
+struct CgRz : SkipNone {  // r.z -> rz (init: p = z) or beta (loop)
+    using value_type = V;
+    const V *r, *z;
+    V *p;
+    template <int W>
+    __device__ __forceinline__ void elem(int64_t i, double (&part)[1]) const {
+        const auto R = ldp<W>(r, i), Z = ldp<W>(z, i);
+#pragma unroll
+        for (int w = 0; w < W; ++w) part[0] = addd(part[0], mulp(R.v[w], Z.v[w]));
+        if (INIT) stp<W>(p, i, Z);
+    }
+    __device__ __forceinline__ void last(Ctl *c, const double (&tot)[1]) const {
+        if (INIT) {
+            c->rz = tot[0];
+            return;
+        }
+        const double rz_new = tot[0];
+        if (!isfinite(rz_new) || c->rz == 0.0) {
+            breakdown(c, c->iter);
+            return;
+        }
+        c->beta = rz_new / c->rz;
+        c->rz = rz_new;
+    }
+};
+
+template <class V>
+struct CgUpdateNoZ : SkipNone {  // x += alpha p; r -= alpha q; r.r -> criteria
+    using value_type = V;
+    const V *p, *q;
+    V *x, *r;
+    double alpha;
+    __device__ __forceinline__ void prepare(const Ctl *c) { alpha = c->alpha; }
+    template <int W>
+    __device__ __forceinline__ void elem(int64_t i, double (&part)[1]) const {
+        const auto P = ldp<W>(p, i), Q = ldp<W>(q, i);
+        auto X = ldp<W>(x, i), R = ldp<W>(r, i);
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            X.v[w] = axpy_e(alpha, P.v[w], X.v[w]);
+            R.v[w] = axpy_e(-alpha, Q.v[w], R.v[w]);
+            part[0] = addd(part[0], mulp(R.v[w], R.v[w]));
+        }
+        stp<W>(x, i, X);
+        stp<W>(r, i, R);
+    }
+    __device__ __forceinline__ void last(Ctl *c, const double (&tot)[1]) const {
+        const int64_t it = c->iter;
+        const double rnorm = sqrt(tot[0]);
+        c->rnorm = rnorm;
+        record(c, it, rnorm);
+        int reason = check_criteria(c, it, rnorm, c->bnorm);
+        if (reason == STOP_NONE && rnorm == 0.0) reason = STOP_RESIDUAL;
+        if (reason != STOP_NONE) finish_with(c, it, reason);
+    }
+};
+
+// validate both factors once (the reference raises at the first apply)
+template <class V, class I>
+sb_status tri_precond_check(const sb_tri_precond &m, sb_error *err, cudaStream_t st);
+
+template <class V, class I>
+sb_status cg_solve_tri(const SolveArgs &a) {
+    sb_error *err = a.err;
+    int64_t n = 0;
+    sb_status s = check_solve_args<V>(a, n);
+    if (s != SB_OK) return s;
+    const sb_tri_precond m = *a.tri;
+    s = tri_precond_check<V, I>(m, err, a.st);
+    if (s != SB_OK) return s;
+    const int64_t cap = a.log->history_cap;
+    SolverWs w = carve_ws(a.ws, SB_SOLVER_CG, sizeof(V), n, 0, cap);
+    V *r = ws_vec<V>(w, 0), *z = ws_vec<V>(w, 1), *p = ws_vec<V>(w, 2), *q = ws_vec<V>(w, 3),
+      *t = ws_vec<V>(w, 4);
+    const V *b = (const V *)a.b->data;
+    V *x = (V *)a.x->data;
+    Ctl *ctl = w.ctl;
+    double *part = w.partials;
+    const sb_matrix M = *a.A;
+    const TriWs tw = carve_tri_ws(m.workspace, n);
+    Ctl h = initial_ctl(*a.crit, w, cap);
+    auto precond = [=](const V *in, cudaStream_t st) -> cudaError_t {  // z = U^{-1} L^{-1} in
+        cudaError_t e = launch_trsv<V, I>(*m.l, true, m.l_unit != 0, in, 1, t, 1, tw, ctl, TRI_SKIP_DONE, st);
+        if (e != cudaSuccess) return e;
+        return launch_trsv<V, I>(*m.u, false, false, t, 1, z, 1, tw, ctl, TRI_SKIP_DONE, st);
+    };
+    LoopSpec spec;
+    spec.key = "cgtri" + std::to_string(sizeof(V)) + std::to_string(sizeof(I)) + "|" + matrix_key(M) +
+               ptr_key({b, x, a.ws, w.vecs, w.hist, m.l->row_ptrs, m.l->values, m.u->row_ptrs, m.u->values,
+                        m.workspace}) + std::to_string(m.l_unit);
+    spec.poll_chunk = 8;
+    spec.setup = [=](cudaStream_t st) -> cudaError_t {
+        cudaError_t e = matrix_apply<V, I>(M, x, 1, t, 1, EpiStore<V>{t, 1}, st);
+        if (e != cudaSuccess) return e;
+        e = launch_ew<2>(n, ctl, part, CgInitNoZ<V>{{}, b, t, r}, st);
+        if (e != cudaSuccess) return e;
+        e = precond(r, st);
+        if (e != cudaSuccess) return e;
+        return launch_ew<1>(n, ctl, part, CgRz<V, true>{{}, r, z, p}, st);
+    };
+    spec.body = [=](cudaStream_t st) -> cudaError_t {
+        cudaError_t e = matrix_apply<V, I>(
+            M, p, 1, q, 1, EpiSolver<V, 1, CgPqFin>{q, p, nullptr, ctl, part, CgPqFin{}}, st);
+        if (e != cudaSuccess) return e;
+        e = launch_ew<1>(n, ctl, part, CgUpdateNoZ<V>{{}, p, q, x, r, 0.0}, st);
+        if (e != cudaSuccess) return e;
+        e = precond(r, st);
+        if (e != cudaSuccess) return e;
+        e = launch_ew<1>(n, ctl, part, CgRz<V, false>{{}, r, z, nullptr}, st);
+        if (e != cudaSuccess) return e;
+        return launch_ew<0>(n, ctl, part, CgDirection<V>{{}, z, p, 0.0}, st);
+    };
+    s = run_loop(spec, ctl, h, a.st, err);
+    if (s != SB_OK) return s;
+    return finish_log(h, a, w);
+}
+
 template <class V, class I>
 sb_status cg_solve(const SolveArgs &a) {
+    if (a.tri) return cg_solve_tri<V, I>(a);
     sb_error *err = a.err;
     int64_t n = 0;
     sb_status s = check_solve_args<V>(a, n);
@@ -625,6 +774,24 @@ int sb_cg_last_loop(void) { return g_cg_last_loop; }
                                         as_stream(stream), err});                                  \
         SB_GUARD_END                                                                               \
     }
+
+#define SB_TRI_DEFS(V, VN, I, IN)                                                                  \
+    sb_status sb_cg_solve_tri_##VN##_##IN(const sb_matrix *a, const sb_tri_precond *m,              \
+                                          const sb_dense *b, sb_dense *x, const sb_criteria *crit,  \
+                                          void *workspace, sb_log *log, sb_stream_t stream,         \
+                                          sb_error *err) {                                          \
+        SB_GUARD_BEGIN                                                                              \
+        if (!m || !m->l || !m->u || !m->workspace)                                                  \
+            return fail(err, SB_ERR_INVALID_ARGUMENT, "triangular preconditioner: null argument");  \
+        SolveArgs sa{a, nullptr, b, x, crit, 0, workspace, log, as_stream(stream), err};            \
+        sa.tri = m;                                                                                 \
+        return cg_solve<V, I>(sa);                                                                  \
+        SB_GUARD_END                                                                                \
+    }
+SB_TRI_DEFS(float, float, int32_t, i32)
+SB_TRI_DEFS(float, float, int64_t, i64)
+SB_TRI_DEFS(double, double, int32_t, i32)
+SB_TRI_DEFS(double, double, int64_t, i64)
 
 SB_DEFS(float, float, int32_t, i32)
 SB_DEFS(float, float, int64_t, i64)

@@ -37,6 +37,22 @@ __device__ __forceinline__ V scal_e(double alpha, V x) {
 // Jacobi apply (np.multiply in the value dtype, precond.py:62)
 __device__ __forceinline__ float vmul(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ double vmul(double a, double b) { return __dmul_rn(a, b); }
+// value-dtype scalar ops of the factorizations (NumPy scalar semantics, precond.py:155-187)
+__device__ __forceinline__ float vdiv(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double vdiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float vsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double vsub(double a, double b) { return __dsub_rn(a, b); }
+
+// first position in [lo, hi) (sorted) whose value is >= key
+template <class T>
+__host__ __device__ __forceinline__ const T *lbound(const T *lo, const T *hi, T key) {
+    while (lo < hi) {
+        const T *mid = lo + (hi - lo) / 2;
+        if (*mid < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
 
 // ------------------------------------------------------------------ cache-policy loads
 // Matrix streams are read exactly once per SpMV: evict-first in L2, no L1 allocation,

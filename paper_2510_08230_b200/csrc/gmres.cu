@@ -3,6 +3,7 @@
 #include <cmath>
 
 #include "solver_common.cuh"
+#include "trisolve.cuh"
 
 namespace sb {
 
@@ -266,6 +267,53 @@ struct GmUpdate : SkipUnlessCycleEnd {
     }
 };
 
+// ILU / IC right preconditioning (_gmres_update with m.apply, solvers.py:311-319): the
+// accumulated V_k y goes to `acc`, two triangular sweeps form dx, then x += dx.
+template <class V>
+struct GmAccum : SkipUnlessCycleEnd {
+    using value_type = V;
+    const V *basis;
+    size_t vstride;
+    V *acc_out;
+    const double *y;
+    int k;
+    __device__ __forceinline__ void prepare(const Ctl *c) {
+        k = c->k;
+        y = c->y;
+    }
+    template <int W>
+    __device__ __forceinline__ void elem(int64_t e, double (&)[1]) const {
+        Pk<V, W> acc;
+#pragma unroll
+        for (int w = 0; w < W; ++w) acc.v[w] = (V)0;
+        for (int i = 0; i < k; ++i) {
+            const auto Vi = ldp<W>(basis + (size_t)i * vstride, e);
+            const double yi = y[i];
+#pragma unroll
+            for (int w = 0; w < W; ++w) acc.v[w] = axpy_e(yi, Vi.v[w], acc.v[w]);
+        }
+        stp<W>(acc_out, e, acc);
+    }
+};
+
+template <class V>
+struct GmAddX : SkipUnlessCycleEnd {  // x = axpy(1.0, dx, x); then finish if a criterion fired
+    using value_type = V;
+    const V *dx;
+    V *x;
+    template <int W>
+    __device__ __forceinline__ void elem(int64_t e, double (&)[1]) const {
+        const auto D = ldp<W>(dx, e);
+        auto X = ldp<W>(x, e);
+#pragma unroll
+        for (int w = 0; w < W; ++w) X.v[w] = axpy_e(1.0, D.v[w], X.v[w]);
+        stp<W>(x, e, X);
+    }
+    __device__ __forceinline__ void last(Ctl *c, const double (&)[1]) const {
+        if (c->finish) finish_with(c, c->iter, c->stop_reason);
+    }
+};
+
 template <class V, class I>
 sb_status gmres_solve(const SolveArgs &a) {
     sb_error *err = a.err;
@@ -287,6 +335,12 @@ sb_status gmres_solve(const SolveArgs &a) {
     Ctl *ctl = w.ctl;
     double *part = w.partials;
     const sb_matrix M = *a.A;
+    const sb_tri_precond *tri = a.tri;
+    if (tri) {
+        s = tri_precond_check<V, I>(*tri, err, a.st);
+        if (s != SB_OK) return s;
+    }
+    const TriWs tw = tri ? carve_tri_ws(tri->workspace, n) : TriWs{};
     Ctl h = initial_ctl(*a.crit, w, cap);
     h.dim = m;
     double *sm = w.small;
@@ -299,6 +353,9 @@ sb_status gmres_solve(const SolveArgs &a) {
     LoopSpec spec;
     spec.key = "gmres" + std::to_string(sizeof(V)) + std::to_string(sizeof(I)) + "|" + std::to_string(m) +
                "|" + matrix_key(M) + ptr_key({a.inv, b, x, a.ws, w.vecs, w.hist, w.small});
+    if (tri)
+        spec.key += "|tri" + std::to_string(tri->l_unit) +
+                    ptr_key({tri->l->row_ptrs, tri->l->values, tri->u->row_ptrs, tri->u->values, tri->workspace});
     spec.poll_chunk = 1;
     spec.setup = [=](cudaStream_t st) -> cudaError_t {
         return launch_ew<1>(n, ctl, part, NormB<V>{{}, b}, st);
@@ -312,7 +369,14 @@ sb_status gmres_solve(const SolveArgs &a) {
         if (e != cudaSuccess) return e;
         for (int64_t j = 0; j < m; ++j) {
             const V *zin = V_(j);
-            if (inv) {
+            if (tri) {  // z = U^{-1} L^{-1} v_j (t is free inside a cycle)
+                e = launch_trsv<V, I>(*tri->l, true, tri->l_unit != 0, V_(j), 1, t, 1, tw, ctl,
+                                      TRI_SKIP_CYCLE_END, st);
+                if (e != cudaSuccess) return e;
+                e = launch_trsv<V, I>(*tri->u, false, false, t, 1, z, 1, tw, ctl, TRI_SKIP_CYCLE_END, st);
+                if (e != cudaSuccess) return e;
+                zin = z;
+            } else if (inv) {
                 e = launch_ew<0>(n, ctl, part, GmPrecond<V>{{}, V_(j), inv, z}, st);
                 if (e != cudaSuccess) return e;
                 zin = z;
@@ -333,6 +397,15 @@ sb_status gmres_solve(const SolveArgs &a) {
         scalar_kernel<<<1, 1, 0, st>>>(ctl, GmBackSub{});
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
+        if (tri) {  // r (free until the next restart) <- V_k y; dx = M^{-1} r; x += dx
+            e = launch_ew<0>(n, ctl, part, GmAccum<V>{{}, basis, vstride, r, nullptr, 0}, st);
+            if (e != cudaSuccess) return e;
+            e = launch_trsv<V, I>(*tri->l, true, tri->l_unit != 0, r, 1, t, 1, tw, ctl, TRI_SKIP_UNLESS_CYCLE_END, st);
+            if (e != cudaSuccess) return e;
+            e = launch_trsv<V, I>(*tri->u, false, false, t, 1, z, 1, tw, ctl, TRI_SKIP_UNLESS_CYCLE_END, st);
+            if (e != cudaSuccess) return e;
+            return launch_ew<1>(n, ctl, part, GmAddX<V>{{}, z, x}, st);
+        }
         return launch_ew<1>(n, ctl, part, GmUpdate<V, 0>{{}, basis, vstride, inv, x, nullptr, 0}, st);
     };
     s = run_loop(spec, ctl, h, a.st, err);
@@ -356,6 +429,25 @@ extern "C" {
                                            as_stream(stream), err});                               \
         SB_GUARD_END                                                                               \
     }
+
+#define SB_TRI_DEFS(V, VN, I, IN)                                                                  \
+    sb_status sb_gmres_solve_tri_##VN##_##IN(const sb_matrix *a, const sb_tri_precond *m,           \
+                                             const sb_dense *b, sb_dense *x,                        \
+                                             const sb_criteria *crit, int64_t krylov_dim,           \
+                                             void *workspace, sb_log *log, sb_stream_t stream,      \
+                                             sb_error *err) {                                       \
+        SB_GUARD_BEGIN                                                                              \
+        if (!m || !m->l || !m->u || !m->workspace)                                                  \
+            return fail(err, SB_ERR_INVALID_ARGUMENT, "triangular preconditioner: null argument");  \
+        SolveArgs sa{a, nullptr, b, x, crit, krylov_dim, workspace, log, as_stream(stream), err};   \
+        sa.tri = m;                                                                                 \
+        return gmres_solve<V, I>(sa);                                                               \
+        SB_GUARD_END                                                                                \
+    }
+SB_TRI_DEFS(float, float, int32_t, i32)
+SB_TRI_DEFS(float, float, int64_t, i64)
+SB_TRI_DEFS(double, double, int32_t, i32)
+SB_TRI_DEFS(double, double, int64_t, i64)
 
 SB_DEFS(float, float, int32_t, i32)
 SB_DEFS(float, float, int64_t, i64)

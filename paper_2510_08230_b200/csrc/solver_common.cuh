@@ -333,6 +333,7 @@ struct SolveArgs {
     sb_log *log;
     cudaStream_t st;
     sb_error *err;
+    const sb_tri_precond *tri = nullptr;  // ILU / IC factors (CG, GMRES), else Jacobi / none
 };
 
 template <class V>

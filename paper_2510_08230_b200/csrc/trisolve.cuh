@@ -1,0 +1,191 @@
+// trisolve.cuh -- sync-free sparse triangular solves on the device, shared by the
+// standalone entry points (trisolve.cu) and the ILU / IC preconditioned solver loops.
+//
+// Reference: _kernels.solve_lower / solve_upper (_kernels.py:91-137) via
+// linop.solve_lower_tri / solve_upper_tri (linop.py:169-198): one sequential sweep;
+// acc = b[i] + 0.0 in fp64, acc -= values[k] * x[j] in stored order (the product in the
+// value dtype), x[i] = acc (unit diagonal) or acc / diag, cast on store.
+//
+// B200 shape: one thread per row, rows claimed in solve order by warps through an
+// atomic counter (so every row a thread waits on belongs to an already running warp:
+// no deadlock whatever the scheduling), a per-row ready flag published with a release
+// store after x[i] and awaited with acquire loads.  Rows whose dependencies are done
+// proceed immediately, so the sweep runs at the matrix's dependency-level parallelism
+// without an analysis phase or one launch per level.  Each row's arithmetic is the
+// reference's, in the reference's order -> bit-exact results.
+#pragma once
+
+#include <algorithm>
+
+#include "capi_util.cuh"
+#include "solver_common.cuh"
+
+namespace sb {
+
+// workspace of one triangular sweep: ready flags (n int32) + claim counter
+struct TriWs {
+    int *ready;
+    unsigned long long *counter;
+    unsigned long long *err;  // first failing row key (factorizations / checks)
+};
+
+inline size_t tri_ws_bytes(int64_t n) { return a256(sizeof(int) * (size_t)(n > 0 ? n : 1)) + 256; }
+
+inline TriWs carve_tri_ws(void *ws, int64_t n) {
+    unsigned char *p = (unsigned char *)ws;
+    TriWs w;
+    w.ready = (int *)p;
+    p += a256(sizeof(int) * (size_t)(n > 0 ? n : 1));
+    w.counter = (unsigned long long *)p;
+    w.err = (unsigned long long *)(p + 64);
+    return w;
+}
+
+__device__ __forceinline__ int ld_acquire_i32(const int *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_i32(int *p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_ready(const int *ready, int64_t j) {
+    while (ld_acquire_i32(ready + j) == 0) {
+    }
+}
+
+// Claims the next 32 rows (in solve order) for the calling warp; all lanes return the
+// same base.  Must be called by the full warp.
+__device__ __forceinline__ int64_t claim_rows(unsigned long long *counter) {
+    unsigned long long base = 0;
+    if ((threadIdx.x & 31) == 0) base = atomicAdd(counter, 32ull);
+    return (int64_t)__shfl_sync(0xffffffffu, base, 0);
+}
+
+// solver-loop skip rule (ctl may be null for standalone sweeps)
+enum { TRI_SKIP_NONE = 0, TRI_SKIP_DONE = 1, TRI_SKIP_CYCLE_END = 2, TRI_SKIP_UNLESS_CYCLE_END = 3 };
+__device__ __forceinline__ bool tri_skip(const Ctl *c, int mode) {
+    if (!c || mode == TRI_SKIP_NONE) return false;
+    if (loop_done(c)) return true;
+    if (mode == TRI_SKIP_CYCLE_END) return c->cycle_end != 0;
+    if (mode == TRI_SKIP_UNLESS_CYCLE_END) return c->cycle_end == 0;
+    return false;
+}
+
+// x = T^{-1} b for a triangular CSR T whose structure was validated (tri_check_kernel)
+template <class V, class I, bool LOWER>
+__global__ void __launch_bounds__(256) sptrsv_kernel(int64_t n, const I *__restrict__ rp,
+                                                     const I *__restrict__ ci, const V *__restrict__ val,
+                                                     const V *b, int64_t ldb, V *x, int64_t ldx, int unit,
+                                                     TriWs w, const Ctl *ctl, int skip_mode) {
+    if (tri_skip(ctl, skip_mode)) return;
+    for (;;) {
+        const int64_t base = claim_rows(w.counter);
+        if (base >= n) return;
+        const int64_t t = base + (threadIdx.x & 31);
+        if (t < n) {
+            const int64_t i = LOWER ? t : n - 1 - t;
+            double acc = (double)b[i * ldb] + 0.0;
+            double diag = 1.0;
+            for (int64_t k = rp[i]; k < (int64_t)rp[i + 1]; ++k) {
+                const int64_t j = ci[k];
+                if (LOWER ? j < i : j > i) {
+                    wait_ready(w.ready, j);
+                    acc = __dsub_rn(acc, mulp(val[k], __ldcg(x + j * ldx)));
+                } else if (j == i) {
+                    diag = (double)val[k];
+                }
+            }
+            x[i * ldx] = (LOWER && unit) ? (V)acc : (V)__ddiv_rn(acc, diag);
+            st_release_i32(w.ready + i, 1);
+        }
+    }
+}
+
+// Structure / diagonal check in solve order (the reference stops at the first failing
+// row): key = position * 4 + kind, kind 1 = entry on the wrong side, 2 = missing or
+// zero diagonal (non-unit).  atomicMin keeps the first failing row.
+template <class V, class I>
+__global__ void __launch_bounds__(256) tri_check_kernel(int64_t n, const I *__restrict__ rp,
+                                                        const I *__restrict__ ci, const V *__restrict__ val,
+                                                        int lower, int unit, unsigned long long *err) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int kind = 0;
+        bool has_diag = false;
+        double diag = 0.0;
+        for (int64_t k = rp[i]; k < (int64_t)rp[i + 1]; ++k) {
+            const int64_t j = ci[k];
+            if (lower ? j > i : j < i) {
+                kind = 1;
+                break;
+            }
+            if (j == i) {
+                has_diag = true;
+                diag = (double)val[k];
+            }
+        }
+        if (kind == 0 && !(lower && unit) && (!has_diag || diag == 0.0)) kind = 2;
+        if (kind) {
+            const unsigned long long pos = lower ? (unsigned long long)i : (unsigned long long)(n - 1 - i);
+            atomicMin(err, pos * 4ull + (unsigned long long)kind);
+        }
+    }
+}
+
+template <class V, class I>
+cudaError_t launch_trsv(const sb_csr &T, bool lower, bool unit, const V *b, int64_t ldb, V *x, int64_t ldx,
+                        const TriWs &w, const Ctl *ctl, int skip_mode, cudaStream_t st) {
+    const int64_t n = T.rows;
+    if (n == 0) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(w.ready, 0, sizeof(int) * (size_t)n, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(w.counter, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    const int grid = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)device_info().sms * 8);
+    if (lower)
+        sptrsv_kernel<V, I, true><<<grid, 256, 0, st>>>(n, (const I *)T.row_ptrs, (const I *)T.col_idxs,
+                                                        (const V *)T.values, b, ldb, x, ldx, unit ? 1 : 0, w,
+                                                        ctl, skip_mode);
+    else
+        sptrsv_kernel<V, I, false><<<grid, 256, 0, st>>>(n, (const I *)T.row_ptrs, (const I *)T.col_idxs,
+                                                         (const V *)T.values, b, ldb, x, ldx, 0, w, ctl,
+                                                         skip_mode);
+    return cudaGetLastError();
+}
+
+// Structure / diagonal check of one factor in solve order, synchronous: returns
+// SB_ERR_NOT_TRIANGULAR / SB_ERR_SINGULAR_TRIANGLE with the reference's row.
+template <class V, class I>
+sb_status tri_factor_check(const sb_csr &T, bool lower, bool unit, const TriWs &w, cudaStream_t st, sb_error *err) {
+    const int64_t n = T.rows;
+    if (n == 0) return SB_OK;
+    SB_CUDA(cudaMemsetAsync(w.err, 0xff, sizeof(unsigned long long), st));
+    const int grid = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)device_info().sms * 8);
+    tri_check_kernel<V, I><<<grid, 256, 0, st>>>(n, (const I *)T.row_ptrs, (const I *)T.col_idxs,
+                                                 (const V *)T.values, lower ? 1 : 0, unit ? 1 : 0, w.err);
+    SB_CUDA(cudaGetLastError());
+    unsigned long long key = 0;
+    SB_CUDA(cudaMemcpyAsync(&key, w.err, sizeof(key), cudaMemcpyDeviceToHost, st));
+    SB_CUDA(cudaStreamSynchronize(st));
+    if (key == ~0ull) return SB_OK;
+    const int64_t pos = (int64_t)(key >> 2), row = lower ? pos : n - 1 - pos;
+    if (err) err->row = row;
+    if ((key & 3) == 1)
+        return fail(err, SB_ERR_NOT_TRIANGULAR, "entry %s the diagonal in row %lld", lower ? "above" : "below",
+                    (long long)row);
+    return fail(err, SB_ERR_SINGULAR_TRIANGLE, "zero or missing diagonal in row %lld", (long long)row);
+}
+
+template <class V, class I>
+sb_status tri_precond_check(const sb_tri_precond &m, sb_error *err, cudaStream_t st) {
+    const int64_t n = m.l->rows;
+    if (m.l->rows != m.l->cols || m.u->rows != m.u->cols || m.u->rows != n)
+        return fail(err, SB_ERR_DIMENSION_MISMATCH, "triangular factors must be square and of one size");
+    const TriWs w = carve_tri_ws(m.workspace, n);
+    sb_status s = tri_factor_check<V, I>(*m.l, true, m.l_unit != 0, w, st, err);
+    if (s != SB_OK) return s;
+    return tri_factor_check<V, I>(*m.u, false, false, w, st, err);
+}
+
+}  // namespace sb

@@ -2,8 +2,8 @@
 
 Same public names as the reference ``sparseops`` (pkg/src/sparseops/__init__.py)
 for the hot path -- devices, dense storage, BLAS-1, CSR/COO storage and conversion,
-LinOp, Jacobi, CG/CGS/GMRES solvers, criteria, config solve -- plus ELL, SELL-P,
-Hybrid and BiCGSTAB.  All compute runs in libsparseb200 on the GPU.
+LinOp, Jacobi, ILU(0)/IC(0) and triangular solves, CG/CGS/GMRES solvers, criteria,
+config solve -- plus ELL, SELL-P, Hybrid and BiCGSTAB.  All compute runs in libsparseb200 on the GPU.
 """
 
 from . import errors
@@ -15,9 +15,10 @@ from .formats import (CooMatrix, CsrMatrix, EllMatrix, HybridMatrix, SellpMatrix
                       coo_from_arrays, coo_from_csr, coo_from_triplets, csr_from_coo,
                       csr_from_dense, ell_from_csr, from_scipy, from_torch, hybrid_ell_width,
                       hybrid_from_csr, sellp_from_csr, validate)
-from .linop import LinOp, apply_advanced
+from .linop import LinOp, apply_advanced, solve_lower_tri, solve_upper_tri
 from .mmio import read_matrix_market, write_matrix_market
-from .precond import JacobiPreconditioner, ic0_factorize, ilu0_factorize, jacobi_create
+from .precond import (IcFactor, IluFactors, JacobiPreconditioner, ic0_factorize, ic_apply,
+                      ilu0_factorize, ilu_apply, jacobi_create)
 from .solvers import (Bicgstab, Cg, Cgs, ConvergenceLog, Gmres, Iteration, ResidualNorm,
                       SolverParams, bicgstab_solve, cg_solve, cgs_solve, check_criteria,
                       gmres_solve, givens_rotation, validate_criteria)

@@ -10,10 +10,13 @@ fused device pass (sb_apply_advanced_*).
 from __future__ import annotations
 
 import abc
+import ctypes
 
+from .. import _lib
 from .core import DenseMatrix, Device, _check_apply_shapes, axpy, copy_into, dense_create, scal
+from .errors import DimensionMismatchError, InvalidArgumentError
 
-__all__ = ["LinOp", "apply_advanced"]
+__all__ = ["LinOp", "apply_advanced", "solve_lower_tri", "solve_upper_tri"]
 
 
 class LinOp(abc.ABC):
@@ -62,3 +65,48 @@ def apply_advanced(op, alpha: float, b: DenseMatrix, beta: float, x: DenseMatrix
         scal(beta, x)
         axpy(alpha, t, x)
     return x
+
+
+# ------------------------------------------------------------------ triangular solves
+_TRI_WS = {}
+
+
+def tri_workspace(device: Device, n: int):
+    """Per-device scratch of the sync-free triangular sweeps (ready flags, counters)."""
+    import torch
+
+    need = int(_lib.fn("sb_tri_workspace_bytes")(n))
+    key = device.id
+    ws = _TRI_WS.get(key)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=device.torch)
+        _TRI_WS[key] = ws
+    return ws
+
+
+def _trisolve(t, b: DenseMatrix, x: DenseMatrix, lower: bool, unit: bool) -> DenseMatrix:
+    from .formats import CsrMatrix, _ptr, _stream
+
+    if not isinstance(t, CsrMatrix):
+        raise InvalidArgumentError(f"triangular solves need CSR storage, got {type(t).__name__}")
+    if t.rows != t.cols:
+        raise DimensionMismatchError(f"triangular solve needs a square matrix, got {t.shape}")
+    _check_apply_shapes(t.shape, b, x)
+    ws = tri_workspace(t.device, t.rows)
+    st, bs, xs = t.struct(), b.struct(), x.struct()
+    _lib.call(f"sb_csr_trisolve_{t._suffix()}", ctypes.byref(st), int(lower), int(unit),
+              ctypes.byref(bs), ctypes.byref(xs), _ptr(ws), _stream(t.device))
+    return x
+
+
+def solve_lower_tri(l, b: DenseMatrix, x: DenseMatrix, unit_diag: bool = False) -> DenseMatrix:
+    """Solve L*x = b by forward substitution (linop.py:169-189); the device sweep keeps the
+    reference's per-row order (bit-exact).  With ``unit_diag`` the diagonal is implicitly
+    1 and stored diagonal entries are ignored as values; entries above the diagonal raise
+    NotTriangularError, a missing / zero diagonal SingularTriangleError (first row)."""
+    return _trisolve(l, b, x, True, unit_diag)
+
+
+def solve_upper_tri(u, b: DenseMatrix, x: DenseMatrix) -> DenseMatrix:
+    """Solve U*x = b by backward substitution (linop.py:192-198)."""
+    return _trisolve(u, b, x, False, False)

@@ -26,7 +26,8 @@ from .errors import (BreakdownError, DimensionMismatchError, InvalidArgumentErro
                      NumericFailureError, PrecisionMismatchError, UnsupportedFeatureError)
 from .formats import _SparseBase, _stream
 from .linop import LinOp
-from .precond import JacobiPreconditioner
+from .precond import IcFactor, IluFactors, JacobiPreconditioner
+from .linop import tri_workspace
 
 __all__ = ["Iteration", "ResidualNorm", "ConvergenceLog", "SolverParams", "check_criteria",
            "validate_criteria", "givens_rotation", "Cg", "Cgs", "Gmres", "Bicgstab",
@@ -184,15 +185,31 @@ class _SolverBase(LinOp):
         if not (a.values.dtype == b.values.dtype == x.values.dtype):
             raise PrecisionMismatchError("matrix, b and x must share one precision")
         m = self.preconditioner
+        tri = None
         if m is None:
             inv = None
         elif isinstance(m, JacobiPreconditioner):
             if m.inv_diag.numel() != n or m.inv_diag.dtype != a.values.dtype:
                 raise DimensionMismatchError("preconditioner does not match the operator")
             inv = m.inv_diag
+        elif isinstance(m, (IluFactors, IcFactor)):
+            if self._kind not in ("cg", "gmres"):
+                raise UnsupportedFeatureError(
+                    f"{type(m).__name__} preconditioning runs in the device CG and GMRES; "
+                    f"use Jacobi with {self._kind}")
+            l, l_unit, u = m.tri_factors()
+            if l.rows != n or u.rows != n or l.values.dtype != a.values.dtype or \
+                    u.values.dtype != a.values.dtype or l.index_width != a.index_width or \
+                    u.index_width != a.index_width:
+                raise DimensionMismatchError("preconditioner factors do not match the operator")
+            inv = None
+            ls, us = l.struct(), u.struct()
+            tws = tri_workspace(a.device, n)
+            tri = (_lib.SbTriPrecond(ctypes.pointer(ls), int(l_unit), 0, ctypes.pointer(us),
+                                     tws.data_ptr()), ls, us, tws)
         else:
             raise UnsupportedFeatureError(
-                f"{type(m).__name__} is not available on the device; use Jacobi or None")
+                f"{type(m).__name__} is not available on the device; use Jacobi, ILU, IC or None")
         # contiguous, 16-byte aligned vectors for the fused kernels (a padded stride or an
         # offset view is copied around)
         bb = b if _packed(b) else _contiguous_copy(b)
@@ -212,7 +229,13 @@ class _SolverBase(LinOp):
                                   STOP_RESIDUAL if log.stop_reason == 0 else STOP_MAX_ITERS)
 
         try:
-            if self._kind == "gmres":
+            if tri is not None:
+                tname = f"sb_{self._kind}_solve_tri_{a._suffix()}"
+                extra = (int(self.krylov_dim),) if self._kind == "gmres" else ()
+                _lib.call(tname, ctypes.byref(mat), ctypes.byref(tri[0]), ctypes.byref(bs),
+                          ctypes.byref(xs), ctypes.byref(crit), *extra,
+                          ctypes.c_void_p(ws.data_ptr()), ctypes.byref(log), _stream(a.device))
+            elif self._kind == "gmres":
                 _lib.call(name, ctypes.byref(mat), inv_p, ctypes.byref(bs), ctypes.byref(xs),
                           ctypes.byref(crit), int(self.krylov_dim), ctypes.c_void_p(ws.data_ptr()),
                           ctypes.byref(log), _stream(a.device))

@@ -14,8 +14,8 @@ from tests.gpu_util import host
 
 pytestmark = pytest.mark.gpu
 
-# Listing 1 of the paper / test_pipeline_example.py:11-37, with the CUDA device and the
-# device Jacobi preconditioner (ILU is outside the B200 hot path)
+# Listing 1 of the paper / test_pipeline_example.py:11-37 verbatim, with the CUDA device:
+# ILU(0)-preconditioned GMRES(30)
 PIPELINE = """
 import paper_2510_08230_b200.pysparseops as pg
 import numpy as np
@@ -32,8 +32,8 @@ x = pg.as_tensor(
   device=dev, dim=(n_rows,1), dtype="double", fill=0.0
 )
 
-# Create Jacobi preconditioner
-preconditioner = pg.preconditioner.Jacobi(dev, mtx)
+# Create ILU preconditioner
+preconditioner = pg.preconditioner.Ilu(dev, mtx)
 
 #Setup GMRES solver
 solver = pg.solver.gmres(dev, mtx, preconditioner,
@@ -65,9 +65,11 @@ def mtx_file(tmp_path, monkeypatch):
     return m
 
 
-def test_listing1_runs_verbatim(mtx_file):
+@pytest.mark.parametrize("precond", ["Ilu", "Jacobi", "Ic"])
+def test_listing1_runs_verbatim(mtx_file, precond):
     ns = {}
-    exec(compile(PIPELINE, "pipeline_example", "exec"), ns)
+    exec(compile(PIPELINE.replace("preconditioner.Ilu(", f"preconditioner.{precond}("),
+                 "pipeline_example", "exec"), ns)
     logger, result, x, b, mtx = ns["logger"], ns["result"], ns["x"], ns["b"], ns["mtx"]
     assert result is x
     assert logger.converged and logger.stop_reason == "residual"
@@ -89,6 +91,10 @@ def test_listing2_config_solve(mtx_file):
     x = pg.as_tensor(device=dev, dim=(mtx.rows, 1), fill=0.0)
     logger, result = pg.solve(args, mtx, b, x)
     assert result is x and logger.converged
+    args["preconditioner"] = {"type": "preconditioner::Ilu"}
+    x2 = pg.as_tensor(device=dev, dim=(mtx.rows, 1), fill=0.0)
+    logger2, _ = pg.solve(args, mtx, b, x2)
+    assert logger2.converged and logger2.stop_reason == "residual"
 
 
 def test_dispatch_reaches_every_instantiation():
