@@ -185,7 +185,23 @@ sb_status spmv_matrix(const sb_matrix &M, const sb_dense *b, sb_dense *x, cudaSt
     if (s != SB_OK) return s;
     if (M.format == SB_FMT_CSR && ((const sb_csr *)M.mat)->nnz > 0 && !((const sb_csr *)M.mat)->plan)
         return fail(err, SB_ERR_INVALID_ARGUMENT, "CSR matrix has no plan");
-    for (int64_t j = 0; j < b->cols; ++j) {
+    int64_t j = 0;
+    if (b->cols > 1 && M.format == SB_FMT_CSR) {  // stream SpMM: the matrix once per 8/4/2 columns
+        const sb_csr &A = *(const sb_csr *)M.mat;
+        if (A.plan && A.plan->kernel == SB_CSR_STREAM && A.rows > 0) {
+            while (b->cols - j >= 2) {
+                const int K = b->cols - j >= 8 ? 8 : (b->cols - j >= 4 ? 4 : 2);
+                const V *bj = (const V *)b->data + j;
+                V *xj = (V *)x->data + j;
+                cudaError_t e = K == 8 ? launch_csr_spmm<V, I, 8>(A, bj, b->stride, xj, x->stride, st)
+                                : K == 4 ? launch_csr_spmm<V, I, 4>(A, bj, b->stride, xj, x->stride, st)
+                                         : launch_csr_spmm<V, I, 2>(A, bj, b->stride, xj, x->stride, st);
+                SB_CUDA(e);
+                j += K;
+            }
+        }
+    }
+    for (; j < b->cols; ++j) {
         const V *bj = (const V *)b->data + j;
         V *xj = (V *)x->data + j;
         SB_CUDA((matrix_apply<V, I>(M, bj, b->stride, xj, x->stride, EpiStore<V>{xj, x->stride}, st)));

@@ -254,6 +254,89 @@ __global__ void __launch_bounds__(R, epi_min_ctas<Epi>(R)) csr_stream_kernel(int
     epi.finish(part);
 }
 
+// ============================================================ CSR: stream SpMM (multi-RHS)
+// x[:, 0:K] = A b[:, 0:K] (b, x row-major with leading dimensions ldb, ldx): the stream
+// kernel's TMA-staged row blocks with K accumulators per thread, so the matrix streams
+// once for K right-hand sides (linop.py:115 applies column by column; each column's sum
+// keeps the same sequential order -> bitwise equal to K single-vector SpMVs).
+template <class V, class I, int R, int K>
+__global__ void __launch_bounds__(R) csr_stream_spmm_kernel(int64_t rows, int64_t nnz, const I *__restrict__ rp,
+                                                            const I *__restrict__ ci, const V *__restrict__ val,
+                                                            const V *__restrict__ b, int64_t ldb, V *x,
+                                                            int64_t ldx, int nnz_cap) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ StreamMeta meta[2];
+    const StreamLayout<V, I> L(R, nnz_cap);
+    const size_t sb = L.stage_bytes();
+    const int tid = threadIdx.x;
+    const int64_t nblk = (rows + R - 1) / R;
+    const uint64_t pol = policy_evict_first();
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    auto issue = [&](int64_t blk, int s) {
+        unsigned char *st = smem + s * sb;
+        V *sv = reinterpret_cast<V *>(st);
+        I *sc = reinterpret_cast<I *>(st + L.off_c());
+        I *sr = reinterpret_cast<I *>(st + L.off_r());
+        const int64_t r0 = blk * R, r1 = r0 + R < rows ? r0 + R : rows;
+        const int64_t k0 = rp[r0], k1 = rp[r1];
+        StreamMeta m;
+        m.r0 = r0;
+        m.r1 = r1;
+        uint32_t bv = stage_range(val, k0, k1, nnz, sv, m.av);
+        uint32_t bc = stage_range(ci, k0, k1, nnz, sc, m.ac);
+        uint32_t br = stage_range(rp, r0, r1 + 1, rows + 1, sr, m.ar);
+        meta[s] = m;
+        mbar_arrive_expect_tx(&bar[s], bv + bc + br);
+        if (bv) bulk_g2s(sv, val + m.av, bv, &bar[s], pol);
+        if (bc) bulk_g2s(sc, ci + m.ac, bc, &bar[s], pol);
+        if (br) bulk_g2s(sr, rp + m.ar, br, &bar[s], pol);
+    };
+    int64_t blk = blockIdx.x;
+    if (tid == 0 && blk < nblk) issue(blk, 0);
+    for (int it = 0; blk < nblk; blk += gridDim.x, ++it) {
+        const int s = it & 1;
+        if (tid == 0 && blk + gridDim.x < nblk) issue(blk + gridDim.x, s ^ 1);
+        mbar_wait(&bar[s], (it >> 1) & 1);
+        const unsigned char *st = smem + s * sb;
+        const V *sv = reinterpret_cast<const V *>(st);
+        const I *sc = reinterpret_cast<const I *>(st + L.off_c());
+        const I *sr = reinterpret_cast<const I *>(st + L.off_r());
+        const StreamMeta m = meta[s];
+        const int64_t i = m.r0 + tid;
+        if (i < m.r1) {
+            const int64_t kb = sr[i - m.ar], ke = sr[i + 1 - m.ar];
+            double acc[K];
+#pragma unroll
+            for (int j = 0; j < K; ++j) acc[j] = 0.0;
+            for (int64_t k = kb; k < ke; k += 4) {
+                V vv[4], bb[4][K];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t kk = k + u < ke ? k + u : ke - 1;
+                    vv[u] = sv[kk - m.av];
+                    const V *bp = b + (int64_t)sc[kk - m.ac] * ldb;
+#pragma unroll
+                    for (int j = 0; j < K; ++j) bb[u][j] = __ldg(bp + j);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (k + u < ke)
+#pragma unroll
+                        for (int j = 0; j < K; ++j) acc[j] = addd(acc[j], mulp(vv[u], bb[u][j]));
+            }
+#pragma unroll
+            for (int j = 0; j < K; ++j) x[i * ldx + j] = (V)acc[j];
+        }
+        __syncthreads();
+    }
+}
+
 // ============================================================ CSR: vector (sub-warp per row)
 // S lanes per row (S in 2..32 chosen from the mean row length), strided partials,
 // fixed shuffle tree.

@@ -74,6 +74,38 @@ cudaError_t launch_csr_stream(const sb_csr &A, const V *b, int64_t ldb, const Ep
                       (const I *)A.col_idxs, (const V *)A.values, b, ldb, cap, epi);
 }
 
+template <class V, class I, int K>
+cudaError_t launch_csr_spmm(const sb_csr &A, const V *b, int64_t ldb, V *x, int64_t ldx, cudaStream_t st) {
+    constexpr int R = 128;
+    const sb_csr_plan &P = *A.plan;
+    const int cap = P.nnz_cap;  // a 128-row block holds at most the nnz of a 128- or 256-row plan block
+    if (P.block_rows < 128) {  // 64-row plans: stage with their own cap at R = 64
+        constexpr int R64 = 64;
+        const size_t smem = 2 * StreamLayout<V, I>(R64, P.nnz_cap).stage_bytes();
+        auto kern = csr_stream_spmm_kernel<V, I, R64, K>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        int grid = persistent_grid(kern, R64, smem);
+        const int64_t nblk = ceil_div(A.rows, R64);
+        if (grid > nblk) grid = (int)nblk;
+        kern<<<grid, R64, smem, st>>>(A.rows, A.nnz, (const I *)A.row_ptrs, (const I *)A.col_idxs,
+                                      (const V *)A.values, b, ldb, x, ldx, P.nnz_cap);
+        return cudaGetLastError();
+    }
+    const size_t smem = 2 * StreamLayout<V, I>(R, cap).stage_bytes();
+    auto kern = csr_stream_spmm_kernel<V, I, R, K>;
+    static int configured = 0;
+    if (!configured) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        configured = 1;
+    }
+    int grid = persistent_grid(kern, R, smem);
+    const int64_t nblk = ceil_div(A.rows, R);
+    if (grid > nblk) grid = (int)nblk;
+    kern<<<grid, R, smem, st>>>(A.rows, A.nnz, (const I *)A.row_ptrs, (const I *)A.col_idxs,
+                                (const V *)A.values, b, ldb, x, ldx, cap);
+    return cudaGetLastError();
+}
+
 template <class V, class I, int S, class Epi>
 cudaError_t launch_csr_vector(const sb_csr &A, const V *b, int64_t ldb, const Epi &epi,
                               cudaStream_t st) {

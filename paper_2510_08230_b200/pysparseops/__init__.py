@@ -19,6 +19,7 @@ SciPy and torch.  Usage::
 from ..sparseops import ConvergenceLog
 from . import bindings, preconditioner, solver
 from .api import axpy, device, dot, matrix, norm2, read, scal, solve, spmv
+from .eigen import rayleigh_ritz
 from .errors import (BindingError, CopyRequiredError, InstantiationMismatchError,
                      NoMatchingInstantiationError, OrthonormalityError)
 from .tensor import Tensor, as_tensor
@@ -26,6 +27,7 @@ from .tensor import Tensor, as_tensor
 __version__ = "0.1.0"
 
 __all__ = ["ConvergenceLog", "Tensor", "as_tensor", "axpy", "bindings", "device", "dot",
-           "matrix", "norm2", "preconditioner", "read", "scal", "solve", "solver", "spmv",
+           "matrix", "norm2", "preconditioner", "rayleigh_ritz", "read", "scal", "solve", "solver",
+           "spmv",
            "BindingError", "CopyRequiredError", "InstantiationMismatchError",
            "NoMatchingInstantiationError", "OrthonormalityError"]

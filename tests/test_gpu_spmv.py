@@ -253,3 +253,25 @@ def test_tile_kernel_edge_cases(dev, vdt):
         # rows of <= 32 entries that do not cross a tile boundary keep the sequential order
         inside = (lens <= 32) & (rp[:-1] // C == np.maximum(rp[1:] - 1, rp[:-1]) // C)
         np.testing.assert_array_equal(got[inside], ref[inside], err_msg=name)
+
+
+def test_stream_spmm_multi_rhs_bitwise(dev):
+    """Multi-RHS apply on stream-CSR matrices uses the SpMM kernel (matrix streamed once
+    per 8 / 4 / 2 columns): every column equals the single-vector SpMV bit for bit,
+    for k = 2..11 (chunk remainders), strided b / x, fp64 and fp32."""
+    rng = np.random.default_rng(31)
+    for prec, vdt in ((sp.Precision.double, np.float64), (sp.Precision.single, np.float32)):
+        a = gen.stencil_csr(dev, 20, dim=3, precision=prec)
+        assert a.kernel == "stream"
+        n = a.rows
+        for k in (2, 3, 5, 8, 11):
+            bm = rng.standard_normal((n, k + 1)).astype(vdt)  # stride k+1: strided view
+            b = sp.dense_from_array(dev, bm.copy())
+            bview = sp.DenseMatrix(dev, n, k, b.values, stride=k + 1)
+            x = out(dev, n, vdt, cols=k)
+            a.apply(bview, x)
+            got = host(x)
+            for j in range(k):
+                y = out(dev, n, vdt)
+                a.apply(vec(dev, bm[:, j]), y)
+                np.testing.assert_array_equal(got[:, j], host(y), err_msg=f"k={k} col={j}")
