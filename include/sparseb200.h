@@ -123,6 +123,11 @@ typedef struct {
     int64_t num_tiles; /* ceil(nnz / sb_coo_tile_entries()) */
     void *carry_rows;  /* int64[num_tiles] */
     void *carry_vals;  /* double[num_tiles] */
+    /* optional row-pointer index of the sorted row array (rows + 1, index width) and a
+       CSR plan over it: set -> the SpMV runs the CSR kernels on (row_ptrs, col_idxs,
+       values) and never re-reads row_idxs; NULL -> segmented-reduction warp kernel */
+    const void *row_ptrs;
+    const sb_csr_plan *csr_plan;
 } sb_coo_plan;
 
 /* formats.CooMatrix (formats.py:57-81): canonical (sorted, unique) entries */

@@ -55,7 +55,8 @@ class SbCsr(ctypes.Structure):
 
 
 class SbCooPlan(ctypes.Structure):
-    _fields_ = [("num_tiles", c_i64), ("carry_rows", c_vp), ("carry_vals", c_vp)]
+    _fields_ = [("num_tiles", c_i64), ("carry_rows", c_vp), ("carry_vals", c_vp),
+                ("row_ptrs", c_vp), ("csr_plan", ctypes.c_void_p)]
 
 
 class SbCoo(ctypes.Structure):

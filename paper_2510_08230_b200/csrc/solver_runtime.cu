@@ -203,7 +203,13 @@ std::string matrix_key(const sb_matrix &M) {
         const sb_coo &A = *(const sb_coo *)M.mat;
         s += ptr_key({A.row_idxs, A.col_idxs, A.values}) + std::to_string(A.rows) + "," +
              std::to_string(A.nnz);
-        if (A.plan) s += ptr_key({A.plan->carry_rows, A.plan->carry_vals}) + std::to_string(A.plan->num_tiles);
+        if (A.plan) {
+            s += ptr_key({A.plan->carry_rows, A.plan->carry_vals, A.plan->row_ptrs}) + std::to_string(A.plan->num_tiles);
+            if (A.plan->csr_plan)
+                s += "|" + std::to_string(A.plan->csr_plan->kernel) + "," + std::to_string(A.plan->csr_plan->block_rows) +
+                     "," + std::to_string(A.plan->csr_plan->nnz_cap) +
+                     ptr_key({A.plan->csr_plan->tile_rows, A.plan->csr_plan->carry_rows});
+        }
         break;
     }
     case SB_FMT_ELL: {

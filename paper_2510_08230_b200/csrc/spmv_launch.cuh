@@ -294,6 +294,12 @@ cudaError_t coo_raw(const sb_coo &A, const V *b, int64_t ldb, V *x, int64_t ldx,
 template <class V, class I, class Epi>
 cudaError_t coo_apply(const sb_coo &A, const V *b, int64_t ldb, V *x_out, int64_t ldx,
                       const Epi &epi, cudaStream_t st) {
+    if (A.plan && A.plan->row_ptrs && A.plan->csr_plan) {
+        // sorted COO rows == CSR rows: run the CSR kernels on the row-pointer index
+        // (bitwise what spmv_coo computes: each row-run summed in stored order)
+        const sb_csr C{A.rows, A.cols, A.nnz, A.plan->row_ptrs, A.col_idxs, A.values, A.plan->csr_plan};
+        return csr_apply<V, I>(C, b, ldb, x_out, ldx, epi, st);
+    }
     if constexpr (epi_has_gather<Epi>::value) return cudaErrorNotSupported;
     cudaError_t e = coo_raw<V, I>(A, b, ldb, x_out, ldx, false, st);
     if (e != cudaSuccess || is_plain_store<Epi>::value) return e;
@@ -425,6 +431,11 @@ inline bool matrix_row_owning(const sb_matrix &M) {
     case SB_FMT_CSR: {
         const sb_csr &A = *(const sb_csr *)M.mat;
         return !A.plan || (A.plan->kernel != SB_CSR_MERGE && A.plan->kernel != SB_CSR_TILE);
+    }
+    case SB_FMT_COO: {  // row-pointer-indexed COO runs the CSR kernels
+        const sb_coo &A = *(const sb_coo *)M.mat;
+        return A.plan && A.plan->row_ptrs && A.plan->csr_plan &&
+               A.plan->csr_plan->kernel != SB_CSR_MERGE && A.plan->csr_plan->kernel != SB_CSR_TILE;
     }
     case SB_FMT_ELL:
     case SB_FMT_SELLP: return true;

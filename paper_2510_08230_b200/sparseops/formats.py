@@ -130,8 +130,11 @@ class CooMatrix(_SparseBase):
 
     _fmt, _fmt_id = "coo", _lib.FMT_COO
 
-    def __init__(self, device: Device, rows, cols, row_idxs, col_idxs, values):
+    def __init__(self, device: Device, rows, cols, row_idxs, col_idxs, values, kernel="auto"):
         self._device = device
+        if kernel not in ("auto", "segmented"):
+            raise InvalidArgumentError(f"unknown COO kernel {kernel!r}; expected 'auto' or 'segmented'")
+        self.kernel_request = kernel
         self.rows, self.cols = int(rows), int(cols)
         self.col_idxs = _on_device(device, col_idxs)
         self.row_idxs = _on_device(device, row_idxs)
@@ -146,13 +149,37 @@ class CooMatrix(_SparseBase):
         self._plan = None
 
     def plan(self) -> _lib.SbCooPlan:
+        """Carry buffers of the segmented warp kernel and, for ``kernel="auto"``, a
+        row-pointer index of the sorted rows with a CSR plan over it: the SpMV then runs
+        the CSR kernels (stream / tile / ...) on (row_ptrs, col_idxs, values) -- the same
+        per-row sums as spmv_coo (linop.py:137-159), without re-reading row_idxs."""
         if self._plan is None:
             tiles = -(-self._nnz // int(_lib.fn("sb_coo_tile_entries")()))
             self._carry_rows = torch.empty(max(tiles, 1), dtype=torch.int64, device=self.device.torch)
             self._carry_vals = torch.empty(max(tiles, 1), dtype=torch.float64, device=self.device.torch)
+            rp_ptr, csr_plan = 0, None
+            if self.kernel_request == "auto" and self.rows > 0 and self._nnz > 0:
+                rp = torch.empty(self.rows + 1, dtype=self.col_idxs.dtype, device=self.device.torch)
+                _lib.call(f"sb_csr_row_ptrs_from_coo_{self.index_width.suffix}", self.rows, self._nnz,
+                          _ptr(self.row_idxs), _ptr(rp), _stream(self.device))
+                self._csr_index = CsrMatrix(self.device, self.rows, self.cols, rp, self.col_idxs,
+                                            self.values)
+                self._csr_plan = self._csr_index.plan()
+                rp_ptr, csr_plan = rp.data_ptr(), ctypes.addressof(self._csr_plan)
             self._plan = _lib.SbCooPlan(tiles, self._carry_rows.data_ptr(),
-                                        self._carry_vals.data_ptr())
+                                        self._carry_vals.data_ptr(), rp_ptr, csr_plan)
         return self._plan
+
+    def with_kernel(self, kernel: str) -> "CooMatrix":
+        """Same arrays (shared), "auto" (row-pointer index + CSR kernels) or "segmented"
+        (the segmented-reduction warp kernel over the row array)."""
+        return CooMatrix(self.device, self.rows, self.cols, self.row_idxs, self.col_idxs,
+                         self.values, kernel=kernel)
+
+    @property
+    def kernel(self) -> str:
+        p = self.plan()
+        return "segmented" if not p.row_ptrs else "csr-" + self._csr_index.kernel
 
     def struct(self) -> _lib.SbCoo:
         return _lib.SbCoo(self.rows, self.cols, self._nnz, _ptr(self.row_idxs).value,
@@ -606,7 +633,8 @@ def hybrid_from_csr(m: CsrMatrix, ell_width: int | None = None,
                     torch.empty(w * stride, dtype=m.values.dtype, device=dev), nnz=m.nnz - t)
     coo = CooMatrix(m.device, m.rows, m.cols, torch.empty(t, dtype=it, device=dev),
                     torch.empty(t, dtype=it, device=dev),
-                    torch.empty(t, dtype=m.values.dtype, device=dev))
+                    torch.empty(t, dtype=m.values.dtype, device=dev),
+                    kernel="segmented")  # the tail accumulates into x: warp kernel
     out = HybridMatrix(m.device, ell, coo)
     st = out.struct()
     src = m.struct()

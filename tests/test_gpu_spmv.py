@@ -49,9 +49,11 @@ def test_coo_ell_sellp_hybrid_on_golden_suite(dev, vdt, idt):
         rows, cols = (int(t) for t in m["shape"])
         a = csr(dev, m["row_ptrs"], m["col_idxs"], m["values"], cols)
         b = vec(dev, m["b"])
-        for fmt in ("coo", "ell", "sellp", "sellp32", "sellp_direct", "hybrid", "hybrid2"):
+        for fmt in ("coo", "coo_seg", "ell", "sellp", "sellp32", "sellp_direct", "hybrid", "hybrid2"):
             if fmt == "coo":
                 mat = sp.coo_from_csr(a)
+            elif fmt == "coo_seg":
+                mat = sp.coo_from_csr(a).with_kernel("segmented")
             elif fmt == "ell":
                 mat = sp.ell_from_csr(a)
             elif fmt == "sellp":
@@ -69,8 +71,9 @@ def test_coo_ell_sellp_hybrid_on_golden_suite(dev, vdt, idt):
             got = host(x)
             if fmt in ("ell", "sellp", "sellp32", "sellp_direct"):
                 np.testing.assert_array_equal(got, m["x"], err_msg=f"{fmt} {rows}x{cols}")
-            elif fmt == "coo":
-                assert_close(got, m["x"], m["row_ptrs"], m["values"], m["b"])
+            elif fmt == "coo" and mat.kernel in ("csr-stream", "csr-strict"):
+                # row-pointer-indexed COO on a sequential-order CSR kernel: bit-exact
+                np.testing.assert_array_equal(got, m["x"], err_msg=f"{fmt} {rows}x{cols}")
             else:
                 assert_close(got, m["x"], m["row_ptrs"], m["values"], m["b"])
 
@@ -173,7 +176,7 @@ def test_heavy_rows_merge_and_coo(dev):
     a = csr(dev, rp, ci, v)
     assert a.kernel == "tile"
     for mat in (a, a.with_kernel("merge"), a.with_kernel("vector"), sp.coo_from_csr(a),
-                sp.hybrid_from_csr(a), sp.sellp_from_csr(a)):
+                sp.coo_from_csr(a).with_kernel("segmented"), sp.hybrid_from_csr(a), sp.sellp_from_csr(a)):
         x = out(dev, n, np.float64)
         mat.apply(vec(dev, bv), x)
         assert_close(host(x), ref, rp, v, bv)
@@ -214,7 +217,8 @@ def test_powerlaw_config3_formats(dev):
         bv = np.random.default_rng(0).random(n).astype(vdt)
         ref = sbref.csr_spmv(rp, ci, v, bv, threads=8)
         assert a.kernel == "tile"
-        for mat in (a, a.with_kernel("merge"), sp.coo_from_csr(a), sp.sellp_from_csr(a),
+        for mat in (a, a.with_kernel("merge"), sp.coo_from_csr(a),
+                    sp.coo_from_csr(a).with_kernel("segmented"), sp.sellp_from_csr(a),
                     sp.hybrid_from_csr(a)):
             x = out(dev, n, vdt)
             mat.apply(vec(dev, bv), x)

@@ -107,7 +107,8 @@ def config2(dev, out, args, threads, flush):
         b = sp.dense_create(dev, a.rows, 1, prec, 1.0)
         x = sp.dense_create(dev, a.rows, 1, prec, 0.0)
         res = {}
-        for name, m in {"csr": a, "coo": sp.coo_from_csr(a), "ell": sp.ell_from_csr(a),
+        for name, m in {"csr": a, "coo": sp.coo_from_csr(a),
+                        "coo_segmented": sp.coo_from_csr(a).with_kernel("segmented"), "ell": sp.ell_from_csr(a),
                         "sellp64": sp.sellp_from_csr(a, 64), "sellp32": sp.sellp_from_csr(a, 32),
                         "hybrid": sp.hybrid_from_csr(a)}.items():
             us = timed_spmv(m, b, x)
@@ -129,7 +130,7 @@ def config3(dev, out, args, threads, flush):
         b = sp.dense_from_array(dev, torch.tensor(bv))
         x = sp.dense_create(dev, a.rows, 1, prec, 0.0)
         mats = {"csr": a, "csr_merge": a.with_kernel("merge"), "csr_vector": a.with_kernel("vector"),
-                "coo": sp.coo_from_csr(a),
+                "coo": sp.coo_from_csr(a), "coo_segmented": sp.coo_from_csr(a).with_kernel("segmented"),
                 "sellp64": sp.sellp_from_csr(a, 64), "hybrid": sp.hybrid_from_csr(a)}
         res = {}
         for name, m in mats.items():
