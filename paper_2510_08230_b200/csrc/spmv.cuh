@@ -151,7 +151,7 @@ __device__ __forceinline__ uint32_t stage_range(const T *g, int64_t lo, int64_t 
     return (uint32_t)((bulk_end - base) * (int64_t)sizeof(T));
 }
 
-template <class V, class I, int R, class Epi>
+template <class V, class I, int R, class Epi, int NS = 2>
 __global__ void __launch_bounds__(R, epi_min_ctas<Epi>(R)) csr_stream_kernel(int64_t rows, int64_t nnz,
                                                        const I *__restrict__ rp,
                                                        const I *__restrict__ ci,
@@ -159,8 +159,9 @@ __global__ void __launch_bounds__(R, epi_min_ctas<Epi>(R)) csr_stream_kernel(int
                                                        const V *__restrict__ b, int64_t ldb,
                                                        int nnz_cap, Epi epi) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bar[2];
-    __shared__ StreamMeta meta[2];
+    static_assert(NS >= 2 && NS <= 4, "stages");
+    __shared__ __align__(8) uint64_t bar[NS];
+    __shared__ StreamMeta meta[NS];
     const StreamLayout<V, I> L(R, nnz_cap);
     const size_t sb = L.stage_bytes();
     const int tid = threadIdx.x;
@@ -168,8 +169,7 @@ __global__ void __launch_bounds__(R, epi_min_ctas<Epi>(R)) csr_stream_kernel(int
     const uint64_t pol = policy_evict_first();
 
     if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+        for (int q = 0; q < NS; ++q) mbar_init(&bar[q], 1);
         mbar_fence_init();
     }
     __syncthreads();
@@ -197,19 +197,24 @@ __global__ void __launch_bounds__(R, epi_min_ctas<Epi>(R)) csr_stream_kernel(int
     // the first block's matrix ranges are immutable: their TMA copies are issued before
     // waiting on the predecessor kernel (programmatic dependent launch)
     int64_t blk = blockIdx.x;
-    if (tid == 0 && blk < nblk) issue(blk, 0);
+    if (tid == 0)
+        for (int q = 0; q < NS - 1; ++q)
+            if (blk + (int64_t)q * gridDim.x < nblk) issue(blk + (int64_t)q * gridDim.x, q);
     pdl_wait();
     pdl_trigger();
     if (epi.skip()) {
-        if (tid == 0 && blk < nblk) mbar_wait(&bar[0], 0);  // no bulk copy outlives the CTA
+        if (tid == 0)  // no bulk copy outlives the CTA
+            for (int q = 0; q < NS - 1; ++q)
+                if (blk + (int64_t)q * gridDim.x < nblk) mbar_wait(&bar[q], 0);
         return;
     }
     epi_prepare(epi);
     double part[Epi::N] = {};
     for (int it = 0; blk < nblk; blk += gridDim.x, ++it) {
-        const int s = it & 1;
-        const uint32_t parity = (it >> 1) & 1;
-        if (tid == 0 && blk + gridDim.x < nblk) issue(blk + gridDim.x, s ^ 1);
+        const int s = it % NS;
+        const uint32_t parity = (it / NS) & 1;
+        if (tid == 0 && blk + (int64_t)(NS - 1) * gridDim.x < nblk)
+            issue(blk + (int64_t)(NS - 1) * gridDim.x, (it + NS - 1) % NS);
         mbar_wait(&bar[s], parity);
         const unsigned char *st = smem + s * sb;
         const V *sv = reinterpret_cast<const V *>(st);

@@ -46,20 +46,17 @@ inline int elem_grid(int64_t work_items) {
 }
 
 // ---------------------------------------------------------------- CSR
-template <class V, class I, int R, class Epi>
-cudaError_t launch_csr_stream(const sb_csr &A, const V *b, int64_t ldb, const Epi &epi,
-                              cudaStream_t st) {
+template <class V, class I, int R, class Epi, int NS>
+cudaError_t launch_csr_stream_ns(const sb_csr &A, const V *b, int64_t ldb, const Epi &epi, cudaStream_t st) {
     const int cap = A.plan->nnz_cap;
     const StreamLayout<V, I> L(R, cap);
-    const size_t smem = 2 * L.stage_bytes();
+    const size_t smem = NS * L.stage_bytes();
     static int configured = 0;
-    static int grid_per_smem[4] = {0, 0, 0, 0};
-    auto kern = csr_stream_kernel<V, I, R, Epi>;
+    auto kern = csr_stream_kernel<V, I, R, Epi, NS>;
     if (!configured) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         configured = 1;
     }
-    (void)grid_per_smem;
     int grid = persistent_grid(kern, R, smem);
     const int64_t nblk = ceil_div(A.rows, R);
     if (grid > nblk) grid = (int)nblk;
@@ -72,6 +69,14 @@ cudaError_t launch_csr_stream(const sb_csr &A, const V *b, int64_t ldb, const Ep
     // block overlaps the predecessor's drain; its predecessors never write the matrix)
     return launch_pdl(kern, grid, R, smem, st, A.rows, A.nnz, (const I *)A.row_ptrs,
                       (const I *)A.col_idxs, (const V *)A.values, b, ldb, cap, epi);
+}
+
+// TMA ring depth: 2 stages.  Measured (tools/tune_stream2.py, 128^3 fp64 R=256 / fp32
+// R=256): 2 stages 36.7 / 32.3 us, 3 stages 41.6 / 33.9 us, 4 stages 50.3 / 36.4 us --
+// deeper rings cost CTAs per SM without adding useful bytes in flight.
+template <class V, class I, int R, class Epi>
+cudaError_t launch_csr_stream(const sb_csr &A, const V *b, int64_t ldb, const Epi &epi, cudaStream_t st) {
+    return launch_csr_stream_ns<V, I, R, Epi, 2>(A, b, ldb, epi, st);
 }
 
 template <class V, class I, int K>
