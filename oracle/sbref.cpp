@@ -17,6 +17,8 @@
 // The restatement is pinned against vectors produced by the reference itself
 // (tests/golden/make_golden.py -> tests/golden/*.npz; tests/test_oracle_golden.py).
 #include <cmath>
+#include <cstdlib>
+#include <string>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -99,9 +101,39 @@ inline int check_criteria(const ref_criteria &c, int64_t it, double res, double 
 
 // ---------------------------------------------------------------- BLAS-1
 // _kernels.dot_range (_kernels.py:44-49) + core.dot (core.py:358-373)
+// Diagnostics only (tools/): SBREF_DOT=neumaier switches every dot to compensated
+// (Neumaier) summation, to separate rounding sensitivity from algorithmic failure.
+inline bool compensated_dots() {
+    static const bool on = [] {
+        const char *e = getenv("SBREF_DOT");
+        return e && std::string(e) == "neumaier";
+    }();
+    return on;
+}
+inline void neumaier(double &s, double &c, double v) {
+    const double t = s + v;
+    c += std::fabs(s) >= std::fabs(v) ? (s - t) + v : (v - t) + s;
+    s = t;
+}
+
 template <class V>
 double dot(int64_t n, const V *x, const V *y, int th) {
     th = std::max(th, 1);
+    if (compensated_dots()) {
+        std::vector<double> ps(th, 0.0), pc(th, 0.0);
+        run_partitioned(th, n, [&](int t, int64_t lo, int64_t hi) {
+            double s = 0.0, c = 0.0;
+            for (int64_t i = lo; i < hi; ++i) neumaier(s, c, mul(x[i], y[i]));
+            ps[t] = s;
+            pc[t] = c;
+        });
+        double s = 0.0, c = 0.0;
+        for (int t = 0; t < th; ++t) {
+            neumaier(s, c, ps[t]);
+            neumaier(s, c, pc[t]);
+        }
+        return s + c;
+    }
     std::vector<double> part(th, 0.0);
     run_partitioned(th, n, [&](int t, int64_t lo, int64_t hi) {
         double acc = 0.0;
