@@ -1,4 +1,11 @@
 // bicgstab.cu -- right-preconditioned BiCGSTAB on the device (recurrence in oracle/sbref.cpp).
+//
+// Every dot of this solver is Neumaier-compensated (CAcc partials, compensated warp / block
+// / grid trees): on the 256^3 convection-diffusion system (config #4) the recurrence is
+// so sensitive to the summation order that plain fp64 tree dots break down at iteration
+// ~170 while near-exact dots follow the exact-arithmetic trajectory and converge (the
+// oracle with compensated dots: 1059 iterations).  The dots are streamed
+// with the vectors, so the extra flops are free in these bandwidth-bound passes.
 #include <cmath>
 
 #include "solver_common.cuh"
@@ -49,19 +56,20 @@ struct BiDirection : SkipNone {
 template <class V>
 struct BiS : SkipNone {
     using value_type = V;
+    using part_type = CAcc;
     const V *r, *v, *inv;
     V *s, *sh;
     double alpha;
     __device__ __forceinline__ void prepare(const Ctl *c) { alpha = c->alpha; }
     template <int W>
-    __device__ __forceinline__ void elem(int64_t i, double (&part)[1]) const {
+    __device__ __forceinline__ void elem(int64_t i, CAcc (&part)[1]) const {
         const auto R = ldp<W>(r, i), Vv = ldp<W>(v, i), D = ldp_or_one<W>(inv, i);
         Pk<V, W> S, SH;
 #pragma unroll
         for (int w = 0; w < W; ++w) {
             S.v[w] = axpy_e(-alpha, Vv.v[w], R.v[w]);
             SH.v[w] = inv ? vmul(S.v[w], D.v[w]) : S.v[w];
-            part[0] = addd(part[0], mulp(S.v[w], S.v[w]));
+            cadd(part[0], mulp(S.v[w], S.v[w]));
         }
         stp<W>(s, i, S);
         stp<W>(sh, i, SH);
@@ -115,6 +123,7 @@ struct BiOmegaFin {
 template <class V>
 struct BiUpdate : SkipEarly {
     using value_type = V;
+    using part_type = CAcc;
     const V *ph, *sh, *s, *t, *rh;
     V *x, *r;
     double alpha, omega;
@@ -123,7 +132,7 @@ struct BiUpdate : SkipEarly {
         omega = c->omega;
     }
     template <int W>
-    __device__ __forceinline__ void elem(int64_t i, double (&part)[2]) const {
+    __device__ __forceinline__ void elem(int64_t i, CAcc (&part)[2]) const {
         const auto PH = ldp<W>(ph, i), SH = ldp<W>(sh, i), S = ldp<W>(s, i), T = ldp<W>(t, i),
                    RH = ldp<W>(rh, i);
         auto X = ldp<W>(x, i);
@@ -132,8 +141,8 @@ struct BiUpdate : SkipEarly {
         for (int w = 0; w < W; ++w) {
             X.v[w] = axpy_e(omega, SH.v[w], axpy_e(alpha, PH.v[w], X.v[w]));
             R.v[w] = axpy_e(-omega, T.v[w], S.v[w]);
-            part[0] = addd(part[0], mulp(R.v[w], R.v[w]));
-            part[1] = addd(part[1], mulp(RH.v[w], R.v[w]));
+            cadd(part[0], mulp(R.v[w], R.v[w]));
+            cadd(part[1], mulp(RH.v[w], R.v[w]));
         }
         stp<W>(x, i, X);
         stp<W>(r, i, R);
@@ -164,6 +173,25 @@ struct BiUpdate : SkipEarly {
     }
 };
 
+// ShadowInit (solver_common.cuh) with compensated dots
+template <class V>
+struct BiShadowInit : ShadowInit<V> {
+    using part_type = CAcc;
+    template <int W>
+    __device__ __forceinline__ void elem(int64_t i, CAcc (&part)[2]) const {
+        const auto B = ldp<W>(this->b, i), T = ldp<W>(this->t, i);
+        Pk<V, W> R;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            R.v[w] = axpy_e(-1.0, T.v[w], B.v[w]);
+            cadd(part[0], mulp(B.v[w], B.v[w]));
+            cadd(part[1], mulp(R.v[w], R.v[w]));
+        }
+        stp<W>(this->r, i, R);
+        stp<W>(this->shadow, i, R);
+    }
+};
+
 template <class V, class I>
 sb_status bicgstab_solve(const SolveArgs &a) {
     sb_error *err = a.err;
@@ -187,18 +215,18 @@ sb_status bicgstab_solve(const SolveArgs &a) {
     spec.setup = [=](cudaStream_t st) -> cudaError_t {
         cudaError_t e = matrix_apply<V, I>(M, x, 1, t, 1, EpiStore<V>{t, 1}, st);
         if (e != cudaSuccess) return e;
-        return launch_ew<2>(n, ctl, part, ShadowInit<V>{{}, b, t, r, rh}, st);
+        return launch_ew<2>(n, ctl, part, BiShadowInit<V>{{{}, b, t, r, rh}}, st);
     };
     spec.body = [=](cudaStream_t st) -> cudaError_t {
         cudaError_t e = launch_ew<0>(n, ctl, part, BiDirection<V>{{}, r, v, inv, p, ph, 0, 0, false}, st);
         if (e != cudaSuccess) return e;
-        e = matrix_apply<V, I>(M, ph, 1, v, 1, EpiSolver<V, 1, BiSigmaFin>{v, rh, nullptr, ctl, part, {}}, st);
+        e = matrix_apply<V, I>(M, ph, 1, v, 1, EpiSolverC<V, 1, BiSigmaFin>{v, rh, nullptr, ctl, part, {}}, st);
         if (e != cudaSuccess) return e;
         e = launch_ew<1>(n, ctl, part, BiS<V>{{}, r, v, inv, sv, sh, 0}, st);
         if (e != cudaSuccess) return e;
         e = launch_ew<1>(n, ctl, part, BiEarlyX<V>{ph, x, 0}, st);
         if (e != cudaSuccess) return e;
-        e = matrix_apply<V, I>(M, sh, 1, t, 1, EpiSolver<V, 2, BiOmegaFin>{t, nullptr, sv, ctl, part, {}}, st);
+        e = matrix_apply<V, I>(M, sh, 1, t, 1, EpiSolverC<V, 2, BiOmegaFin>{t, nullptr, sv, ctl, part, {}}, st);
         if (e != cudaSuccess) return e;
         return launch_ew<2>(n, ctl, part, BiUpdate<V>{{}, ph, sh, sv, t, rh, x, r, 0, 0}, st);
     };

@@ -210,6 +210,97 @@ __device__ __forceinline__ bool grid_reduce(double (&v)[N], double *partials, un
     return true;
 }
 
+// ------------------------------------------------------------------ compensated sums
+// Neumaier-compensated partial (s + c): used where a recurrence is sensitive enough to
+// the summation order of its dots that only near-exact dots follow the exact-arithmetic
+// trajectory (BiCGSTAB on config #4).  Deterministic like the plain path.
+struct CAcc {
+    double s, c;
+};
+__device__ __forceinline__ void cadd(CAcc &a, double v) {
+    const double t = __dadd_rn(a.s, v);
+    const double e = fabs(a.s) >= fabs(v) ? __dadd_rn(__dsub_rn(a.s, t), v) : __dadd_rn(__dsub_rn(v, t), a.s);
+    a.c = __dadd_rn(a.c, e);
+    a.s = t;
+}
+__device__ __forceinline__ void cmerge(CAcc &a, const CAcc &b) {
+    cadd(a, b.s);
+    a.c = __dadd_rn(a.c, b.c);
+}
+__device__ __forceinline__ double cvalue(const CAcc &a) { return __dadd_rn(a.s, a.c); }
+
+template <int N>
+__device__ __forceinline__ void block_reduce_c(CAcc (&v)[N], CAcc (*scratch)[N]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            CAcc b;
+            b.s = __shfl_down_sync(0xffffffffu, v[k].s, o);
+            b.c = __shfl_down_sync(0xffffffffu, v[k].c, o);
+            cmerge(v[k], b);
+        }
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < N; ++k) scratch[warp][k] = v[k];
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) v[k] = lane < nw ? scratch[lane][k] : CAcc{0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                CAcc b;
+                b.s = __shfl_down_sync(0xffffffffu, v[k].s, o);
+                b.c = __shfl_down_sync(0xffffffffu, v[k].c, o);
+                cmerge(v[k], b);
+            }
+    }
+}
+
+// grid_reduce with compensated partials: partials layout [2N][gridDim.x] (s then c)
+template <int N>
+__device__ __forceinline__ bool grid_reduce(CAcc (&v)[N], double *partials, unsigned *ticket, double (&tot)[N]) {
+    __shared__ CAcc scratch[32][N];
+    __shared__ bool s_last;
+    __shared__ double s_tot[N];
+    block_reduce_c<N>(v, scratch);
+    const int G = gridDim.x;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            partials[(2 * k) * G + blockIdx.x] = v[k].s;
+            partials[(2 * k + 1) * G + blockIdx.x] = v[k].c;
+        }
+        __threadfence();
+        unsigned t = atomicAdd(ticket, 1u);
+        s_last = (t == (unsigned)G - 1);
+    }
+    __syncthreads();
+    if (!s_last) return false;
+    __threadfence();
+    CAcc a[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        a[k] = CAcc{0.0, 0.0};
+        for (int i = threadIdx.x; i < G; i += blockDim.x)
+            cmerge(a[k], CAcc{__ldcg(partials + (2 * k) * G + i), __ldcg(partials + (2 * k + 1) * G + i)});
+    }
+    block_reduce_c<N>(a, scratch);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) s_tot[k] = cvalue(a[k]);
+        *ticket = 0u;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < N; ++k) tot[k] = s_tot[k];
+    return true;
+}
+
 // ------------------------------------------------------------------ launch geometry
 struct DeviceInfo {
     int sms = 148;

@@ -158,13 +158,24 @@ __device__ __forceinline__ void stp(V *p, int64_t i, const Pk<V, W> &r) {
 // block by Op::last.  Fixed grid -> fixed summation order.
 inline int solver_grid() { return device_info().sms * 8; }
 
+// partial type of an elementwise op's fused dots: double, or CAcc if the op declares
+// `using part_type = CAcc;` (compensated, see common.cuh)
+template <class O, class = void>
+struct op_part {
+    using type = double;
+};
+template <class O>
+struct op_part<O, std::void_t<typename O::part_type>> {
+    using type = typename O::part_type;
+};
+
 template <int N, int W, class Op>
 __global__ void __launch_bounds__(256) ew_kernel(int64_t n, Ctl *ctl, double *partials, Op op) {
     pdl_wait();
     pdl_trigger();
     if (loop_done(ctl) || op.skip(ctl)) return;
     op.prepare(ctl);
-    double part[N > 0 ? N : 1] = {};
+    typename op_part<Op>::type part[N > 0 ? N : 1] = {};
     const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t npk = n / W;
@@ -209,6 +220,29 @@ struct EpiSolver {
         if constexpr (N > 1) part[1] = addd(part[1], mulp(u1[i], yi));
     }
     __device__ __forceinline__ void finish(double (&part)[N]) const {
+        double tot[N];
+        if (grid_reduce<N>(part, partials, &ctl->ticket[0], tot) && threadIdx.x == 0) fin.last(ctl, tot);
+    }
+};
+
+// EpiSolver with compensated fused dots
+template <class V, int NDOT, class Fin>
+struct EpiSolverC {
+    static constexpr int N = NDOT;
+    using part_type = CAcc;
+    V *y;
+    const V *u0, *u1;
+    Ctl *ctl;
+    double *partials;
+    Fin fin;
+    __device__ __forceinline__ bool skip() const { return loop_done(ctl) || fin.skip(ctl); }
+    __device__ __forceinline__ void row(int64_t i, double acc, CAcc (&part)[N]) const {
+        const V yi = (V)acc;
+        y[i] = yi;
+        cadd(part[0], u0 ? mulp(u0[i], yi) : mulp(yi, yi));
+        if constexpr (N > 1) cadd(part[1], mulp(u1[i], yi));
+    }
+    __device__ __forceinline__ void finish(CAcc (&part)[N]) const {
         double tot[N];
         if (grid_reduce<N>(part, partials, &ctl->ticket[0], tot) && threadIdx.x == 0) fin.last(ctl, tot);
     }

@@ -57,6 +57,19 @@ constexpr int epi_min_ctas(int R) {
     return epi_min_threads<Epi>::value / R;  // 0 = unspecified (the compiler's own heuristic)
 }
 
+// partial-sum type of an epilogue's fused dots: double, or CAcc (compensated) when the
+// epilogue declares `using part_type = CAcc;`
+template <class E, class = void>
+struct epi_part {
+    using type = double;
+};
+template <class E>
+struct epi_part<E, std::void_t<typename E::part_type>> {
+    using type = typename E::part_type;
+};
+template <class E>
+using epi_part_t = typename epi_part<E>::type;
+
 template <class Epi, class V>
 __device__ __forceinline__ V gather_b(const Epi &e, const V *__restrict__ b, int64_t off) {
     if constexpr (epi_has_gather<Epi>::value) return e.gather(off);
@@ -89,7 +102,7 @@ __global__ void __launch_bounds__(256) csr_strict_kernel(int64_t rows, const I *
                                                          Epi epi) {
     if (epi.skip()) return;
     epi_prepare(epi);
-    double part[Epi::N] = {};
+    epi_part_t<Epi> part[Epi::N] = {};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows;
          i += (int64_t)gridDim.x * blockDim.x) {
         double acc = 0.0;
@@ -209,7 +222,7 @@ __global__ void __launch_bounds__(R, epi_min_ctas<Epi>(R)) csr_stream_kernel(int
         return;
     }
     epi_prepare(epi);
-    double part[Epi::N] = {};
+    epi_part_t<Epi> part[Epi::N] = {};
     for (int it = 0; blk < nblk; blk += gridDim.x, ++it) {
         const int s = it % NS;
         const uint32_t parity = (it / NS) & 1;
@@ -353,7 +366,7 @@ __global__ void __launch_bounds__(256) csr_vector_kernel(int64_t rows, const I *
                                                          Epi epi) {
     if (epi.skip()) return;
     epi_prepare(epi);
-    double part[Epi::N] = {};
+    epi_part_t<Epi> part[Epi::N] = {};
     const int lane = threadIdx.x % S;
     const int64_t group = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / S;
     const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / S;
@@ -1206,7 +1219,7 @@ __global__ void __launch_bounds__(256) ell_kernel(int64_t rows, int64_t width, i
                                                   const V *__restrict__ b, int64_t ldb, Epi epi) {
     if (epi.skip()) return;
     epi_prepare(epi);
-    double part[Epi::N] = {};
+    epi_part_t<Epi> part[Epi::N] = {};
     const int64_t groups = (rows + RPT - 1) / RPT;
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < groups;
          g += (int64_t)gridDim.x * blockDim.x) {
@@ -1234,7 +1247,7 @@ __global__ void __launch_bounds__(256) sellp_kernel(int64_t rows, int64_t S,
                                                     const V *__restrict__ b, int64_t ldb, Epi epi) {
     if (epi.skip()) return;
     epi_prepare(epi);
-    double part[Epi::N] = {};
+    epi_part_t<Epi> part[Epi::N] = {};
     const int64_t nslices = (rows + S - 1) / S;
     const int64_t groups = nslices * (S / RPT);
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < groups;
@@ -1319,7 +1332,7 @@ __global__ void __launch_bounds__(128) sellp_stream_kernel(int64_t rows, int64_t
         if (bv) bulk_g2s(sv, val + bv_base, bv, &bar[st], pol);
         if (bc) bulk_g2s(sc, col + bc_base, bc, &bar[st], pol);
     };
-    double part[Epi::N] = {};
+    epi_part_t<Epi> part[Epi::N] = {};
     int64_t blk = blockIdx.x;
     if (tid == 0 && blk < nblk) issue(blk, 0);
     for (int it = 0; blk < nblk; blk += gridDim.x, ++it) {
@@ -1384,7 +1397,7 @@ __global__ void __launch_bounds__(256) epilogue_pass_kernel(int64_t rows, const 
                                                             Epi epi) {
     if (epi.skip()) return;
     epi_prepare(epi);
-    double part[Epi::N] = {};
+    epi_part_t<Epi> part[Epi::N] = {};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows;
          i += (int64_t)gridDim.x * blockDim.x)
         epi.row(i, (double)x[i * ldx], part);

@@ -322,3 +322,22 @@ def test_graph_cache_tracks_workspace_layout(dev, kind):
                                    err_msg=f"{kind} max_iters={its}")
         if its < 3000:
             assert log.iterations == its
+
+
+@pytest.mark.slow
+def test_config4_bicgstab_converges(dev):
+    """BASELINE config #4: BiCGSTAB + Jacobi on the 256^3 convection-diffusion system.  The
+    recurrence's residual grows by ~20 orders of magnitude before it recovers, so only
+    near-exact dots follow the exact-arithmetic trajectory: the device's compensated dots
+    converge within the oracle's envelope (1045 with 8-chunk sequential sums, 1059 with
+    compensated sums; tests/golden/oracle_probe_256.json)."""
+    import json
+    import os
+    with open(os.path.join(golden_io.GOLDEN, "oracle_probe_256.json")) as fh:
+        probe = json.load(fh)["config4_convdiff3d_256_c0.5_jacobi_rtol1e-8"]
+    lo = min(probe["bicgstab"]["iterations"], probe["bicgstab_compensated_dots"]["iterations"])
+    hi = max(probe["bicgstab"]["iterations"], probe["bicgstab_compensated_dots"]["iterations"])
+    a = gen.convdiff3d(dev, 256)
+    log, _, _ = solve(dev, "bicgstab", a, np.ones(a.rows), [sp.Iteration(5000), sp.ResidualNorm(1e-8)])
+    assert log.converged and log.stop_reason == "residual"
+    assert within_envelope(log.iterations, (lo, hi)), (log.iterations, lo, hi)
