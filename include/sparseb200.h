@@ -146,11 +146,14 @@ typedef struct {
 
 /* SELL-P(slice_size): entry k of row i (slice s = i / S) at (slice_sets[s] + k)*S + i%S.
  * max_block_entries: max stored entries of any 128/S consecutive slices (aligned), for the
- * TMA-staged kernel (0 = use the direct kernel). */
+ * TMA-staged kernel (0 = use the direct kernel).
+ * row_perm (SELL-C-sigma, optional): stored row i holds matrix row row_perm[i] (rows sorted
+ * by length inside windows of sigma rows); NULL = identity (plain SELL-P). */
 typedef struct {
     int64_t rows, cols, slice_size, num_slices;
     const void *slice_lengths, *slice_sets, *col_idxs, *values;
     int64_t max_block_entries;
+    const void *row_perm;
 } sb_sellp;
 
 /* Hybrid(w): the first min(len_i, w) entries of each row in ELL(w), the rest in COO */

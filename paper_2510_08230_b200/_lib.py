@@ -72,7 +72,7 @@ class SbEll(ctypes.Structure):
 class SbSellp(ctypes.Structure):
     _fields_ = [("rows", c_i64), ("cols", c_i64), ("slice_size", c_i64), ("num_slices", c_i64),
                 ("slice_lengths", c_vp), ("slice_sets", c_vp), ("col_idxs", c_vp),
-                ("values", c_vp), ("max_block_entries", c_i64)]
+                ("values", c_vp), ("max_block_entries", c_i64), ("row_perm", c_vp)]
 
 
 class SbHybrid(ctypes.Structure):

@@ -220,7 +220,7 @@ std::string matrix_key(const sb_matrix &M) {
     }
     case SB_FMT_SELLP: {
         const sb_sellp &A = *(const sb_sellp *)M.mat;
-        s += ptr_key({A.slice_lengths, A.slice_sets, A.col_idxs, A.values}) + std::to_string(A.rows) +
+        s += ptr_key({A.slice_lengths, A.slice_sets, A.col_idxs, A.values, A.row_perm}) + std::to_string(A.rows) +
              "," + std::to_string(A.slice_size);
         break;
     }

@@ -1244,7 +1244,8 @@ __global__ void __launch_bounds__(256) sellp_kernel(int64_t rows, int64_t S,
                                                     const I *__restrict__ slice_sets,
                                                     const I *__restrict__ col,
                                                     const V *__restrict__ val,
-                                                    const V *__restrict__ b, int64_t ldb, Epi epi) {
+                                                    const V *__restrict__ b, int64_t ldb, Epi epi,
+                                                    const I *__restrict__ perm) {
     if (epi.skip()) return;
     epi_prepare(epi);
     epi_part_t<Epi> part[Epi::N] = {};
@@ -1262,7 +1263,7 @@ __global__ void __launch_bounds__(256) sellp_kernel(int64_t rows, int64_t S,
         padded_rows<V, I, RPT>(epi, val, col, b, ldb, off, S, len, acc);
 #pragma unroll
         for (int r = 0; r < RPT; ++r)
-            if (i0 + r < rows) epi.row(i0 + r, acc[r], part);
+            if (i0 + r < rows) epi.row(perm ? (int64_t)perm[i0 + r] : i0 + r, acc[r], part);
     }
     epi.finish(part);
 }
@@ -1287,7 +1288,8 @@ __global__ void __launch_bounds__(128) sellp_stream_kernel(int64_t rows, int64_t
                                                            const I *__restrict__ col,
                                                            const V *__restrict__ val,
                                                            const V *__restrict__ b, int64_t ldb,
-                                                           int cap_entries, Epi epi) {
+                                                           int cap_entries, Epi epi,
+                                                           const I *__restrict__ perm) {
     constexpr int SPB = 128 / S;
     static_assert(SPB >= 1 && SPB <= 4, "slice size 32, 64 or 128");
     if (epi.skip()) return;
@@ -1383,7 +1385,7 @@ __global__ void __launch_bounds__(128) sellp_stream_kernel(int64_t rows, int64_t
                 for (int u = 0; u < 8; ++u)
                     if (cc[u] >= 0) acc = addd(acc, mulp(vv[u], bb[u]));
             }
-            epi.row(i, acc, part);
+            epi.row(perm ? (int64_t)perm[i] : i, acc, part);
         }
         __syncthreads();
     }

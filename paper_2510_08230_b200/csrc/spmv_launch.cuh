@@ -360,7 +360,7 @@ cudaError_t launch_sellp_stream(const sb_sellp &A, const V *b, int64_t ldb, cons
     if (grid > nblk) grid = (int)nblk;
     kern<<<grid, 128, 2 * stage, st>>>(A.rows, A.num_slices, (const I *)A.slice_lengths,
                                        (const I *)A.slice_sets, (const I *)A.col_idxs,
-                                       (const V *)A.values, b, ldb, cap, epi);
+                                       (const V *)A.values, b, ldb, cap, epi, (const I *)A.row_perm);
     return cudaGetLastError();
 }
 
@@ -387,7 +387,7 @@ cudaError_t sellp_apply(const sb_sellp &A, const V *b, int64_t ldb, const Epi &e
         if (grid > need) grid = (int)(need > 0 ? need : 1);
         kern<<<grid, 256, 0, st>>>(A.rows, A.slice_size, (const I *)A.slice_lengths,
                                    (const I *)A.slice_sets, (const I *)A.col_idxs,
-                                   (const V *)A.values, b, ldb, epi);
+                                   (const V *)A.values, b, ldb, epi, (const I *)A.row_perm);
     } else {
         auto kern = sellp_kernel<V, I, 1, Epi>;
         int grid = persistent_grid(kern, 256, 0);
@@ -395,7 +395,7 @@ cudaError_t sellp_apply(const sb_sellp &A, const V *b, int64_t ldb, const Epi &e
         if (grid > need) grid = (int)(need > 0 ? need : 1);
         kern<<<grid, 256, 0, st>>>(A.rows, A.slice_size, (const I *)A.slice_lengths,
                                    (const I *)A.slice_sets, (const I *)A.col_idxs,
-                                   (const V *)A.values, b, ldb, epi);
+                                   (const V *)A.values, b, ldb, epi, (const I *)A.row_perm);
     }
     return cudaGetLastError();
 }

@@ -345,8 +345,10 @@ class SellpMatrix(_SparseBase):
     _fmt, _fmt_id = "sellp", _lib.FMT_SELLP
 
     def __init__(self, device, rows, cols, slice_size, slice_lengths, slice_sets, col_idxs,
-                 values, nnz=None):
+                 values, nnz=None, row_perm=None):
         self._device = device
+        # SELL-C-sigma: stored row i holds matrix row row_perm[i] (None: identity)
+        self.row_perm = None if row_perm is None else _on_device(device, row_perm)
         self.rows, self.cols = int(rows), int(cols)
         self.slice_size = int(slice_size)
         self.slice_lengths = _on_device(device, slice_lengths)
@@ -364,7 +366,8 @@ class SellpMatrix(_SparseBase):
     def with_staging(self, staged: bool) -> "SellpMatrix":
         """Same arrays (shared), staged (TMA) or direct SpMV kernel."""
         m = SellpMatrix(self.device, self.rows, self.cols, self.slice_size, self.slice_lengths,
-                        self.slice_sets, self.col_idxs, self.values, nnz=self._nnz)
+                        self.slice_sets, self.col_idxs, self.values, nnz=self._nnz,
+                        row_perm=self.row_perm)
         m.staged = staged
         return m
 
@@ -384,7 +387,8 @@ class SellpMatrix(_SparseBase):
         return _lib.SbSellp(self.rows, self.cols, self.slice_size, self.num_slices,
                             _ptr(self.slice_lengths).value, _ptr(self.slice_sets).value,
                             _ptr(self.col_idxs).value, _ptr(self.values).value,
-                            self.max_block_entries if self.staged else 0)
+                            self.max_block_entries if self.staged else 0,
+                            _ptr(self.row_perm).value if self.row_perm is not None else None)
 
     @property
     def stored(self) -> int:
@@ -406,7 +410,10 @@ class SellpMatrix(_SparseBase):
             vals.append(blk_v[k, l])
         if not rows:
             return np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0)
-        return np.concatenate(rows), np.concatenate(cols), np.concatenate(vals)
+        r = np.concatenate(rows)
+        if self.row_perm is not None:
+            r = self.row_perm.cpu().numpy().astype(np.int64)[r]
+        return r, np.concatenate(cols), np.concatenate(vals)
 
     def __repr__(self):
         return (f"SellpMatrix({self.rows}x{self.cols}, S={self.slice_size}, "
@@ -582,10 +589,21 @@ def ell_from_csr(m: CsrMatrix, stride_align: int = 32, width: int | None = None)
     return out
 
 
-def sellp_from_csr(m: CsrMatrix, slice_size: int = 64) -> SellpMatrix:
-    """CSR -> SELL-P(slice_size) with stride factor 1 and no row sorting."""
+def sellp_from_csr(m: CsrMatrix, slice_size: int = 64, sigma: int = 1) -> SellpMatrix:
+    """CSR -> SELL-P(slice_size) with stride factor 1.  ``sigma`` > 1 gives SELL-C-sigma:
+    rows sorted by decreasing length (stably) inside windows of ``sigma`` rows (a multiple
+    of slice_size) so each slice pads to similar lengths; the kernels write row results
+    through the permutation, and every row keeps its stored entry order (results equal
+    plain SELL-P / CSR bit for bit)."""
     if slice_size < 1:
         raise InvalidArgumentError("slice_size must be positive")
+    if sigma > 1:
+        if sigma % slice_size:
+            raise InvalidArgumentError("sigma must be a multiple of slice_size")
+        perm = _sigma_permutation(m, sigma)
+        out = sellp_from_csr(_permute_rows(m, perm), slice_size)
+        out.row_perm = perm.to(m.col_idxs.dtype)
+        return out
     dev = m.device.torch
     ns = -(-m.rows // slice_size)
     it = m.col_idxs.dtype
@@ -603,6 +621,28 @@ def sellp_from_csr(m: CsrMatrix, slice_size: int = 64) -> SellpMatrix:
     _lib.call(f"sb_sellp_from_csr_{m._suffix()}", ctypes.byref(src), ctypes.byref(st),
               _stream(m.device))
     return out
+
+
+def _sigma_permutation(m: CsrMatrix, sigma: int) -> torch.Tensor:
+    """Rows sorted by decreasing length inside consecutive windows of sigma rows (stable)."""
+    lens = (m.row_ptrs[1:] - m.row_ptrs[:-1]).long()
+    n = m.rows
+    window = torch.arange(n, device=lens.device) // sigma
+    key = window * (int(lens.max()) + 1 if n else 1) + (lens.max() - lens if n else lens)
+    return torch.sort(key, stable=True).indices
+
+
+def _permute_rows(m: CsrMatrix, perm: torch.Tensor) -> CsrMatrix:
+    """Row-permuted copy of m (row p of the result = row perm[p] of m), entries in order."""
+    rp = m.row_ptrs.long()
+    lens = (rp[1:] - rp[:-1])[perm]
+    new_rp = torch.zeros(m.rows + 1, dtype=torch.int64, device=rp.device)
+    torch.cumsum(lens, 0, out=new_rp[1:])
+    start = torch.repeat_interleave(rp[:-1][perm], lens)
+    offs = torch.arange(int(new_rp[-1]), device=rp.device) - torch.repeat_interleave(new_rp[:-1], lens)
+    src = start + offs
+    it = m.col_idxs.dtype
+    return CsrMatrix(m.device, m.rows, m.cols, new_rp.to(it), m.col_idxs[src], m.values[src])
 
 
 def hybrid_ell_width(row_lengths, quantile: float = 0.8) -> int:

@@ -138,7 +138,9 @@ def test_every_format_same_iterations(dev, kind):
     base, _, _ = solve(dev, kind, a, np.ones(a.rows), crit, precond=m)
     assert base.converged and within_envelope(base.iterations, env), (base.iterations, env)
     mats = [a.with_kernel("strict"), a.with_kernel("vector"), a.with_kernel("merge"),
-            sp.coo_from_csr(a), sp.ell_from_csr(a), sp.sellp_from_csr(a), sp.hybrid_from_csr(a, 5)]
+            a.with_kernel("tile"), sp.coo_from_csr(a), sp.coo_from_csr(a).with_kernel("segmented"),
+            sp.ell_from_csr(a), sp.sellp_from_csr(a), sp.sellp_from_csr(a, 32, sigma=256),
+            sp.hybrid_from_csr(a, 5)]
     for mat in mats:
         log, _, _ = solve(dev, kind, mat, np.ones(a.rows), crit, precond=m)
         assert log.converged and within_envelope(log.iterations, env), \

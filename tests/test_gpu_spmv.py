@@ -49,7 +49,8 @@ def test_coo_ell_sellp_hybrid_on_golden_suite(dev, vdt, idt):
         rows, cols = (int(t) for t in m["shape"])
         a = csr(dev, m["row_ptrs"], m["col_idxs"], m["values"], cols)
         b = vec(dev, m["b"])
-        for fmt in ("coo", "coo_seg", "ell", "sellp", "sellp32", "sellp_direct", "hybrid", "hybrid2"):
+        for fmt in ("coo", "coo_seg", "ell", "sellp", "sellp32", "sellp_direct", "sellp_sigma",
+                    "sellp_sigma_direct", "hybrid", "hybrid2"):
             if fmt == "coo":
                 mat = sp.coo_from_csr(a)
             elif fmt == "coo_seg":
@@ -62,6 +63,10 @@ def test_coo_ell_sellp_hybrid_on_golden_suite(dev, vdt, idt):
                 mat = sp.sellp_from_csr(a, 32)
             elif fmt == "sellp_direct":
                 mat = sp.sellp_from_csr(a, 64).with_staging(False)
+            elif fmt == "sellp_sigma":
+                mat = sp.sellp_from_csr(a, 32, sigma=128)
+            elif fmt == "sellp_sigma_direct":
+                mat = sp.sellp_from_csr(a, 32, sigma=64).with_staging(False)
             elif fmt == "hybrid":
                 mat = sp.hybrid_from_csr(a)
             else:
@@ -69,7 +74,7 @@ def test_coo_ell_sellp_hybrid_on_golden_suite(dev, vdt, idt):
             x = out(dev, rows, m["values"].dtype)
             mat.apply(b, x)
             got = host(x)
-            if fmt in ("ell", "sellp", "sellp32", "sellp_direct"):
+            if fmt in ("ell", "sellp", "sellp32", "sellp_direct", "sellp_sigma", "sellp_sigma_direct"):
                 np.testing.assert_array_equal(got, m["x"], err_msg=f"{fmt} {rows}x{cols}")
             elif fmt == "coo" and mat.kernel in ("csr-stream", "csr-strict"):
                 # row-pointer-indexed COO on a sequential-order CSR kernel: bit-exact
@@ -219,7 +224,7 @@ def test_powerlaw_config3_formats(dev):
         assert a.kernel == "tile"
         for mat in (a, a.with_kernel("merge"), sp.coo_from_csr(a),
                     sp.coo_from_csr(a).with_kernel("segmented"), sp.sellp_from_csr(a),
-                    sp.hybrid_from_csr(a)):
+                    sp.sellp_from_csr(a, 64, sigma=8192), sp.hybrid_from_csr(a)):
             x = out(dev, n, vdt)
             mat.apply(vec(dev, bv), x)
             assert_close(host(x), ref, rp, v, bv)

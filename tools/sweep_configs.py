@@ -131,7 +131,8 @@ def config3(dev, out, args, threads, flush):
         x = sp.dense_create(dev, a.rows, 1, prec, 0.0)
         mats = {"csr": a, "csr_merge": a.with_kernel("merge"), "csr_vector": a.with_kernel("vector"),
                 "coo": sp.coo_from_csr(a), "coo_segmented": sp.coo_from_csr(a).with_kernel("segmented"),
-                "sellp64": sp.sellp_from_csr(a, 64), "hybrid": sp.hybrid_from_csr(a)}
+                "sellp64": sp.sellp_from_csr(a, 64),
+                "sellp64_sigma8192": sp.sellp_from_csr(a, 64, sigma=8192), "hybrid": sp.hybrid_from_csr(a)}
         res = {}
         for name, m in mats.items():
             us = timed_spmv(m, b, x)
