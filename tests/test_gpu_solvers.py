@@ -343,3 +343,24 @@ def test_config4_bicgstab_converges(dev):
     log, _, _ = solve(dev, "bicgstab", a, np.ones(a.rows), [sp.Iteration(5000), sp.ResidualNorm(1e-8)])
     assert log.converged and log.stop_reason == "residual"
     assert within_envelope(log.iterations, (lo, hi)), (log.iterations, lo, hi)
+
+
+@pytest.mark.parametrize("kind", ["cg", "gmres", "bicgstab", "cgs"])
+def test_int64_indices_identical(dev, kind):
+    """i64 index instantiations (persistent CG, graph loops, ILU path) give bitwise the same
+    runs as i32: the index width never enters the arithmetic."""
+    c = 0.0 if kind == "cg" else 0.5
+    runs = []
+    for iw in (sp.IndexWidth.i32, sp.IndexWidth.i64):
+        a = gen.stencil_csr(dev, 14, dim=3, c=c, index_width=iw)
+        log, x, _ = solve(dev, kind, a, np.ones(a.rows), [sp.Iteration(2000), sp.ResidualNorm(1e-8)])
+        runs.append((log, x))
+        if kind in ("cg", "gmres"):
+            xi = out(dev, a.rows, np.float64, fill=0.0)
+            li = SOLVERS[kind](a, criteria=[sp.Iteration(2000), sp.ResidualNorm(1e-8)],
+                               preconditioner=sp.ilu0_factorize(a)).solve(vec(dev, np.ones(a.rows)), xi)
+            runs.append((li, host(xi)))
+    half = len(runs) // 2
+    for (l32, x32), (l64, x64) in zip(runs[:half], runs[half:]):
+        assert l32.iterations == l64.iterations and l32.residual_history == l64.residual_history
+        np.testing.assert_array_equal(x32, x64)
