@@ -609,178 +609,15 @@ struct TileLayout {
     static constexpr size_t STAGE = (OFF_R + (size_t)(RCAP + 1 + 2 * VI) * sizeof(I) + 15) & ~size_t(15);
 };
 
-// Three-stage software pipeline, one block barrier per tile: iteration i issues the TMA
-// copy of tile i+1, issues the gathers of tile i, reduces the rows of tile i-1 (whose
-// products are in shared memory) while those gathers are in flight, then multiplies and
-// stores tile i's products.  The row phase is warp-local: lanes sum their rows of <= 32
-// products, rows with longer segments are reduced by the whole warp (ballot loop).
-template <class V, class I, int NT, int C, int RCAP>
-__global__ void __launch_bounds__(NT) csr_tile_kernel(int64_t rows, int64_t nnz, const I *__restrict__ rp,
-                                                      const I *__restrict__ ci, const V *__restrict__ val,
-                                                      const V *__restrict__ b, int64_t ldb, V *x, int64_t ldx,
-                                                      const int64_t *__restrict__ first_row, int64_t ntiles,
-                                                      int64_t *crow, double *cval) {
-    using L = TileLayout<V, I, C, RCAP>;
-    constexpr int PER = C / NT;
-    static_assert(C % NT == 0, "tile size");
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bar[3];
-    __shared__ TileMeta s_meta[3];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t pol = policy_evict_first();
-    const int64_t G = gridDim.x, bid = blockIdx.x;
-    if (tid == 0) {
-        for (int k = 0; k < 3; ++k) mbar_init(&bar[k], 1);
-        mbar_fence_init();
-    }
-    __syncthreads();
-    auto issue = [&](int64_t t, int64_t r0, int64_t r1, int s) {  // thread 0
-        unsigned char *st = smem + s * L::STAGE;
-        V *sv = reinterpret_cast<V *>(st);
-        I *sc = reinterpret_cast<I *>(st + L::OFF_C);
-        I *sr = reinterpret_cast<I *>(st + L::OFF_R);
-        const int64_t k0 = t * C, k1 = k0 + C < nnz ? k0 + C : nnz;
-        int64_t bv0, bc0, br0 = 0;
-        const uint32_t bv = stage_range(val, k0, k1, nnz, sv, bv0);
-        const uint32_t bc = stage_range(ci, k0, k1, nnz, sc, bc0);
-        const bool srp = RCAP > 0 && r1 - r0 <= RCAP;
-        const uint32_t br = srp ? stage_range(rp, r0, r1 + 1, rows + 1, sr, br0) : 0;
-        s_meta[s] = TileMeta{r0, r1, k0 - bv0, k0 - bc0, r0 - br0, srp};
-        mbar_arrive_expect_tx(&bar[s], bv + bc + br);
-        if (bv) bulk_g2s(sv, val + bv0, bv, &bar[s], pol);
-        if (bc) bulk_g2s(sc, ci + bc0, bc, &bar[s], pol);
-        if (br) bulk_g2s(sr, rp + br0, br, &bar[s], pol);
-    };
-    int64_t nr0 = 0, nr1 = 0;  // thread 0: row range of the next tile to issue
-    if (tid == 0 && bid < ntiles) {
-        issue(bid, first_row[bid], first_row[bid + 1], 0);
-        if (bid + G < ntiles) {
-            nr0 = first_row[bid + G];
-            nr1 = first_row[bid + G + 1];
-        }
-    }
-    for (int64_t i = 0;; ++i) {
-        const int64_t t = bid + i * G, tp = t - G;
-        const bool prod = t < ntiles, red = i > 0 && tp < ntiles;
-        if (!prod && !red) break;
-        if (tid == 0 && t + G < ntiles) {  // stage (i+1)%3 last held tile i-2, reduced at i-1
-            issue(t + G, nr0, nr1, (int)((i + 1) % 3));
-            if (t + 2 * G < ntiles) {
-                nr0 = first_row[t + 2 * G];
-                nr1 = first_row[t + 2 * G + 1];
-            }
-        }
-        // ---- gathers of tile t (consumed after the row phase)
-        const int s = (int)(i % 3);
-        V bb[PER];
-        int cnt = 0;
-        V *sv = nullptr;
-        if (prod) {
-            mbar_wait(&bar[s], (uint32_t)((i / 3) & 1));
-            unsigned char *st = smem + s * L::STAGE;
-            const TileMeta m = s_meta[s];
-            sv = reinterpret_cast<V *>(st) + m.dv;
-            const I *sc = reinterpret_cast<const I *>(st + L::OFF_C) + m.dc;
-            const int64_t k0 = t * C;
-            cnt = (int)((k0 + C < nnz ? k0 + C : nnz) - k0);
-#pragma unroll
-            for (int u = 0; u < PER; ++u) {
-                const int j = tid + u * NT;
-                bb[u] = __ldg(b + (int64_t)sc[j < cnt ? j : cnt - 1] * ldb);
-            }
-        }
-        // ---- rows of tile tp (products in stage (i-1)%3)
-        if (red) {
-            const int sp = (int)((i + 2) % 3);
-            unsigned char *st = smem + sp * L::STAGE;
-            const TileMeta m = s_meta[sp];
-            const V *pv = reinterpret_cast<const V *>(st) + m.dv;
-            const I *sr = reinterpret_cast<const I *>(st + L::OFF_R) + m.dr;  // sr[i - r0] = rp[i]
-            const int64_t r0 = m.r0, r1 = m.r1, k0 = tp * C, k1 = k0 + C < nnz ? k0 + C : nnz;
-            auto rpa = [&](int64_t r) -> int64_t {  // rp[r] for r0 <= r <= r1
-                if (r >= rows) return nnz;
-                return m.staged_rp ? (int64_t)sr[r - r0] : (int64_t)__ldg(rp + r);
-            };
-            auto warp_sum = [&](int kb, int ke) -> double {  // lane-strided partials, fixed tree
-                double acc = 0.0;
-                for (int k = kb + lane; k < ke; k += 32) acc = addd(acc, (double)pv[k]);
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) acc = addd(acc, __shfl_down_sync(0xffffffffu, acc, o));
-                return acc;  // valid in lane 0
-            };
-            if (warp == 0) {  // lead segment (row started before the tile) and empty slots
-                const int64_t lead_end = rpa(r0);
-                if (lead_end > k0) {
-                    const double acc = warp_sum(0, (int)((lead_end < k1 ? lead_end : k1) - k0));
-                    if (lane == 0) {
-                        crow[2 * tp] = r0 - 1;
-                        cval[2 * tp] = acc;
-                    }
-                } else if (lane == 0) {
-                    crow[2 * tp] = -1;
-                }
-                if (lane == 0 && !(r1 > r0 && rpa(r1) > k1)) crow[2 * tp + 1] = -1;
-            }
-            for (int64_t base = r0 + warp * 32; base < r1; base += NT) {
-                const int64_t r = base + lane;
-                int kb = 0, ke = 0;
-                bool cont = false;
-                if (r < r1) {
-                    const int64_t a = rpa(r), e = rpa(r + 1);
-                    kb = (int)(a - k0);
-                    ke = (int)((e < k1 ? e : k1) - k0);
-                    cont = e > k1;
-                    if (ke - kb <= 32) {
-                        double acc = 0.0;
-                        for (int k = kb; k < ke; ++k) acc = addd(acc, (double)pv[k]);
-                        if (!cont) {
-                            x[r * ldx] = (V)acc;
-                        } else {  // the tile's last row continues: trail record
-                            crow[2 * tp + 1] = r;
-                            cval[2 * tp + 1] = acc;
-                        }
-                    }
-                }
-                unsigned lm = __ballot_sync(0xffffffffu, r < r1 && ke - kb > 32);
-                while (lm) {
-                    const int j = __ffs(lm) - 1;
-                    lm &= lm - 1;
-                    const int jb = __shfl_sync(0xffffffffu, kb, j), je = __shfl_sync(0xffffffffu, ke, j);
-                    const bool jc = __shfl_sync(0xffffffffu, cont, j);
-                    const double acc = warp_sum(jb, je);
-                    if (lane == 0) {
-                        if (!jc) {
-                            x[(base + j) * ldx] = (V)acc;
-                        } else {
-                            crow[2 * tp + 1] = base + j;
-                            cval[2 * tp + 1] = acc;
-                        }
-                    }
-                }
-            }
-        }
-        // ---- products of tile t, in place
-        if (prod) {
-#pragma unroll
-            for (int u = 0; u < PER; ++u) {
-                const int j = tid + u * NT;
-                if (j < cnt) sv[j] = (V)mulp(sv[j], bb[u]);
-            }
-        }
-        __syncthreads();  // tile t's products complete; stage (i-1)%3 free for reissue
-    }
-}
-
-// Two-stage variant (no row/product overlap, three block barriers per tile, smaller
-// shared footprint -> one more CTA per SM).  Measured faster for fp64 (config #3: 404
-// vs 497 us), slower for fp32 (556 vs 416 us): launch_csr_tile picks per value type.
+// Per tile: wait for the stage, products (barrier), owned rows by threads with long
+// segments queued (barrier), queued segments by warps, record slots (barrier).
 struct TileJob {
     int32_t rel;     // owned-row index relative to first_row[t], or -1 for the lead segment
     int32_t kb, ke;  // product range in the tile
 };
 
 template <class V, class I, int NT, int C, int RCAP>
-__global__ void __launch_bounds__(NT) csr_tile2_kernel(int64_t rows, int64_t nnz, const I *__restrict__ rp,
+__global__ void __launch_bounds__(NT) csr_tile_kernel(int64_t rows, int64_t nnz, const I *__restrict__ rp,
                                                        const I *__restrict__ ci, const V *__restrict__ val,
                                                        const V *__restrict__ b, int64_t ldb, V *x, int64_t ldx,
                                                        const int64_t *__restrict__ first_row, int64_t ntiles,

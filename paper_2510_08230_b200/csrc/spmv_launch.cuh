@@ -162,12 +162,12 @@ cudaError_t launch_csr_merge(const sb_csr &A, const V *b, int64_t ldb, V *x, int
                            (const double *)P.carry_vals, x, ldx, st);
 }
 
-template <class V, class I, int NT, int C, int RCAP, int STAGES>
+template <class V, class I, int NT, int C, int RCAP>
 cudaError_t launch_csr_tile_t(const sb_csr &A, const V *b, int64_t ldb, V *x, int64_t ldx, cudaStream_t st) {
     const sb_csr_plan &P = *A.plan;
     const int64_t ntiles = P.num_tiles / 2;
-    constexpr size_t smem = STAGES * TileLayout<V, I, C, RCAP>::STAGE;
-    auto kern = STAGES == 3 ? csr_tile_kernel<V, I, NT, C, RCAP> : csr_tile2_kernel<V, I, NT, C, RCAP>;
+    constexpr size_t smem = 2 * TileLayout<V, I, C, RCAP>::STAGE;
+    auto kern = csr_tile_kernel<V, I, NT, C, RCAP>;
     static int configured = 0;
     if (!configured) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -186,25 +186,19 @@ cudaError_t launch_csr_tile_t(const sb_csr &A, const V *b, int64_t ldb, V *x, in
     return cudaGetLastError();
 }
 
-// Tile shape per value type, measured on config #3 (tools/tile_ab.py, us per SpMV):
-// fp64 two-stage 2048 404 / pipelined 2048 497 / merge-path 561; fp32 pipelined 2048 416 /
-// two-stage 2048 556 / merge-path 452.  SPARSEB200_TILE_C (1024 / 2048 / 4096) and
-// SPARSEB200_TILE_STAGES (2 / 3) override for experiments.
+// Tile shape (threads x nonzeros per tile), measured on config #3 (tools/tile_ab.py, us per
+// SpMV, merge-path 566 / 452): fp64 256 x 2048 404 (512 x 2048 435, 256 x 1024 416,
+// 256 x 4096 ~600); fp32 512 x 2048 384 (256 x 2048 417, 256 x 1024 400); a three-stage
+// ring overlapping the row sums of tile t-1 with the gathers of tile t was tried and
+// measured slower (fp64 497 us: its extra stage costs a CTA per SM).  SPARSEB200_TILE_C
+// (1024 / 2048 / 4096) overrides the tile size for experiments.
 template <class V, class I>
 cudaError_t launch_csr_tile(const sb_csr &A, const V *b, int64_t ldb, V *x, int64_t ldx, cudaStream_t st) {
-    static const int stages = [] {
-        const char *e = getenv("SPARSEB200_TILE_STAGES");
-        return e ? atoi(e) : (sizeof(V) == 8 ? 2 : 3);
-    }();
     const int64_t C = A.plan->items_per_tile;
-    if (stages == 2) {
-        if (C == 1024) return launch_csr_tile_t<V, I, 128, 1024, 512, 2>(A, b, ldb, x, ldx, st);
-        if (C == 4096) return launch_csr_tile_t<V, I, 256, 4096, 2048, 2>(A, b, ldb, x, ldx, st);
-        return launch_csr_tile_t<V, I, 256, 2048, 1024, 2>(A, b, ldb, x, ldx, st);
-    }
-    if (C == 1024) return launch_csr_tile_t<V, I, 128, 1024, 512, 3>(A, b, ldb, x, ldx, st);
-    if (C == 4096) return launch_csr_tile_t<V, I, 256, 4096, 2048, 3>(A, b, ldb, x, ldx, st);
-    return launch_csr_tile_t<V, I, 256, 2048, 1024, 3>(A, b, ldb, x, ldx, st);
+    if (C == 1024) return launch_csr_tile_t<V, I, 256, 1024, 512>(A, b, ldb, x, ldx, st);
+    if (C == 4096) return launch_csr_tile_t<V, I, 256, 4096, 2048>(A, b, ldb, x, ldx, st);
+    if (sizeof(V) == 4) return launch_csr_tile_t<V, I, 512, 2048, 1024>(A, b, ldb, x, ldx, st);
+    return launch_csr_tile_t<V, I, 256, 2048, 1024>(A, b, ldb, x, ldx, st);
 }
 
 template <class V>
