@@ -1105,21 +1105,21 @@ __global__ void __launch_bounds__(256) sellp_kernel(int64_t rows, int64_t S,
     epi.finish(part);
 }
 
-// ============================================================ SELL-P: TMA-staged slices
+// ============================================================ SELL-P: TMA-staged slice blocks
 // A block of SPB = 128 / S consecutive slices is one contiguous range of the value and
 // column arrays ((slice_sets[s0] .. slice_sets[s0 + SPB]) * S entries), so it is staged
 // exactly like a CSR stream block: one elected thread issues cp.async.bulk copies into a
 // two-stage shared-memory ring (mbarrier completion), the next block is prefetched
 // while this one is reduced, and thread t reduces row t of the block sequentially
 // (column-major within the slice) -> bit-exact with the reference's row order.
-struct SellpMeta {
+struct SellpBlockMeta {
     int64_t s0;              // first slice of the block
     int64_t dv, dc;          // stage slot of the block's first entry (values / columns)
     int32_t len[4], off[4];  // per slice: length, first entry relative to the block start
 };
 
 template <class V, class I, int S, class Epi>
-__global__ void __launch_bounds__(128) sellp_stream_kernel(int64_t rows, int64_t nslices,
+__global__ void __launch_bounds__(128) sellp_block_kernel(int64_t rows, int64_t nslices,
                                                            const I *__restrict__ sl,
                                                            const I *__restrict__ ss,
                                                            const I *__restrict__ col,
@@ -1133,7 +1133,7 @@ __global__ void __launch_bounds__(128) sellp_stream_kernel(int64_t rows, int64_t
     epi_prepare(epi);
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar[2];
-    __shared__ SellpMeta meta[2];
+    __shared__ SellpBlockMeta meta[2];
     constexpr int VV = 16 / sizeof(V), VI = 16 / sizeof(I);
     const size_t cap_v = (size_t)cap_entries + 2 * VV, cap_c = (size_t)cap_entries + 2 * VI;
     const size_t off_c = (cap_v * sizeof(V) + 15) & ~size_t(15);
@@ -1154,7 +1154,7 @@ __global__ void __launch_bounds__(128) sellp_stream_kernel(int64_t rows, int64_t
         I *sc = reinterpret_cast<I *>(p + off_c);
         const int64_t s0 = blk * SPB, s1 = s0 + SPB < nslices ? s0 + SPB : nslices;
         const int64_t lo = (int64_t)ss[s0] * S, hi = (int64_t)ss[s1] * S;
-        SellpMeta m;
+        SellpBlockMeta m;
         m.s0 = s0;
         int64_t bv_base = 0, bc_base = 0;
         const uint32_t bv = stage_range(val, lo, hi, total, sv, bv_base);
@@ -1182,7 +1182,7 @@ __global__ void __launch_bounds__(128) sellp_stream_kernel(int64_t rows, int64_t
         const unsigned char *p = smem + st * stage_bytes;
         const V *sv = reinterpret_cast<const V *>(p);
         const I *sc = reinterpret_cast<const I *>(p + off_c);
-        const SellpMeta m = meta[st];
+        const SellpBlockMeta m = meta[st];
         const int j = tid / S, l = tid % S;
         const int64_t i = (m.s0 + j) * S + l;
         if (j < SPB && i < rows) {
@@ -1225,6 +1225,148 @@ __global__ void __launch_bounds__(128) sellp_stream_kernel(int64_t rows, int64_t
             epi.row(perm ? (int64_t)perm[i] : i, acc, part);
         }
         __syncthreads();
+    }
+    epi.finish(part);
+}
+
+// ============================================================ SELL-P: TMA-staged chunks
+// Blocks whose stored entries exceed the stage (long slices) use this variant.  A block
+// of SPB = 128 / S consecutive slices is one contiguous range of the value and column
+// arrays ((slice_sets[s0] .. slice_sets[s0 + SPB]) * S entries).  It is streamed
+// through a two-stage shared-memory ring in chunks of at most cap_entries entries (a
+// multiple of S, i.e. whole columns): one elected thread issues the cp.async.bulk copies
+// of the next chunk (mbarrier completion) while the current one is reduced.  Thread t
+// owns row t of the block and accumulates its columns chunk by chunk in stored
+// (column-major) order -> bit-exact with the reference's row sum.  Chunking keeps long
+// slices (power-law rows: a 64-row slice of 11,668 columns) streaming instead of
+// falling back to the direct kernel.
+struct SellpMeta {
+    int64_t s0;              // first slice of the block
+    int64_t lo;              // block's first entry (global)
+    int64_t clo, chi;        // this chunk's entries [clo, chi) (global)
+    int64_t bv, bc;          // global entry index held by stage slot 0 (values / columns)
+    int32_t len[4], off[4];  // per slice: length, first entry relative to lo
+    int32_t last;            // last chunk of the block: emit the rows
+};
+
+template <class V, class I, int S, class Epi>
+__global__ void __launch_bounds__(128) sellp_chunk_kernel(int64_t rows, int64_t nslices,
+                                                           const I *__restrict__ sl,
+                                                           const I *__restrict__ ss,
+                                                           const I *__restrict__ col,
+                                                           const V *__restrict__ val,
+                                                           const V *__restrict__ b, int64_t ldb,
+                                                           int cap_entries, Epi epi,
+                                                           const I *__restrict__ perm) {
+    constexpr int SPB = 128 / S;
+    static_assert(SPB >= 1 && SPB <= 4, "slice size 32, 64 or 128");
+    if (epi.skip()) return;
+    epi_prepare(epi);
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ SellpMeta meta[2];
+    constexpr int VV = 16 / sizeof(V), VI = 16 / sizeof(I);
+    const size_t cap_v = (size_t)cap_entries + 2 * VV, cap_c = (size_t)cap_entries + 2 * VI;
+    const size_t off_c = (cap_v * sizeof(V) + 15) & ~size_t(15);
+    const size_t stage_bytes = (off_c + cap_c * sizeof(I) + 15) & ~size_t(15);
+    const int64_t chunk = (int64_t)(cap_entries / S) * S;  // whole columns per chunk
+    const int tid = threadIdx.x;
+    const int64_t nblk = (nslices + SPB - 1) / SPB;
+    const int64_t total = (int64_t)ss[nslices] * S;
+    const uint64_t pol = policy_evict_first();
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    // thread 0: stage chunk [clo, min(clo + chunk, hi)) of block blk; returns true if it
+    // was the block's last chunk, else sets clo to the next chunk's start
+    auto issue = [&](int64_t blk, int64_t &clo, int st) -> bool {
+        unsigned char *p = smem + st * stage_bytes;
+        V *sv = reinterpret_cast<V *>(p);
+        I *sc = reinterpret_cast<I *>(p + off_c);
+        const int64_t s0 = blk * SPB, s1 = s0 + SPB < nslices ? s0 + SPB : nslices;
+        const int64_t lo = (int64_t)ss[s0] * S, hi = (int64_t)ss[s1] * S;
+        if (clo < lo) clo = lo;
+        const int64_t chi = clo + chunk < hi ? clo + chunk : hi;
+        SellpMeta m;
+        m.s0 = s0;
+        m.lo = lo;
+        m.clo = clo;
+        m.chi = chi;
+        m.last = chi == hi;
+        const uint32_t bv = stage_range(val, clo, chi, total, sv, m.bv);
+        const uint32_t bc = stage_range(col, clo, chi, total, sc, m.bc);
+        for (int j = 0; j < SPB; ++j) {
+            const int64_t s = s0 + j;
+            m.len[j] = s < s1 ? (int32_t)sl[s] : 0;
+            m.off[j] = s < s1 ? (int32_t)((int64_t)ss[s] * S - lo) : 0;
+        }
+        meta[st] = m;
+        mbar_arrive_expect_tx(&bar[st], bv + bc);
+        if (bv) bulk_g2s(sv, val + m.bv, bv, &bar[st], pol);
+        if (bc) bulk_g2s(sc, col + m.bc, bc, &bar[st], pol);
+        clo = chi;
+        return chi == hi;
+    };
+    epi_part_t<Epi> part[Epi::N] = {};
+    int64_t blk = blockIdx.x;
+    // the next work item to issue: (nblk_i, nclo); chunks of a block in order, then the
+    // CTA's next block
+    int64_t nb = blk, nclo = -1;
+    if (tid == 0 && blk < nblk && issue(blk, nclo, 0)) {
+        nb = blk + gridDim.x;
+        nclo = -1;
+    }
+    double acc = 0.0;
+    for (int it = 0; blk < nblk; ++it) {
+        const int st = it & 1;
+        const uint32_t parity = (it >> 1) & 1;
+        if (tid == 0 && nb < nblk && issue(nb, nclo, st ^ 1)) {  // prefetch the next chunk
+            nb += gridDim.x;
+            nclo = -1;
+        }
+        mbar_wait(&bar[st], parity);
+        const unsigned char *p = smem + st * stage_bytes;
+        const V *sv = reinterpret_cast<const V *>(p);
+        const I *sc = reinterpret_cast<const I *>(p + off_c);
+        const SellpMeta &m = meta[st];  // read in place (no local copy of the arrays)
+        const int j = tid / S, l = tid % S;
+        const int64_t i = (m.s0 + j) * S + l;
+        const bool last = m.last;
+        if (j < SPB && i < rows) {
+            const int len = m.len[j];
+            const int64_t lo = m.lo, off = m.off[j];
+            // columns of slice j inside this chunk (chunk bounds are whole columns)
+            const int64_t rel0 = m.clo - lo - off, rel1 = m.chi - lo - off;
+            int k = rel0 > 0 ? (int)(rel0 / S) : 0;
+            const int kend = rel1 <= 0 ? 0 : (int)(rel1 / S < len ? rel1 / S : len);
+            const int64_t ov = lo + off + l - m.bv, oc = lo + off + l - m.bc;  // stage slots of k = 0
+            for (; k < kend; k += 8) {
+                V vv[8], bb[8];
+                I cc[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {  // branch-free tail (see csr_stream_kernel)
+                    const int kk = k + u < kend ? k + u : kend - 1;
+                    vv[u] = sv[ov + (int64_t)kk * S];
+                    cc[u] = k + u < kend ? sc[oc + (int64_t)kk * S] : (I)-1;
+                    if constexpr (epi_has_gather<Epi>::value)  // padding: col 0, masked below
+                        bb[u] = gather_b(epi, b, (int64_t)(cc[u] >= 0 ? cc[u] : 0) * ldb);
+                    else
+                        bb[u] = cc[u] >= 0 ? __ldg(b + (int64_t)cc[u] * ldb) : (V)0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (cc[u] >= 0) acc = addd(acc, mulp(vv[u], bb[u]));
+            }
+            if (last) {
+                epi.row(perm ? (int64_t)perm[i] : i, acc, part);
+                acc = 0.0;
+            }
+        }
+        if (last) blk += gridDim.x;
+        __syncthreads();  // stage st consumed before it is re-issued
     }
     epi.finish(part);
 }

@@ -3,6 +3,7 @@
 #pragma once
 
 #include "../../include/sparseb200.h"
+#include <algorithm>
 #include <cstdlib>
 
 #include "spmv.cuh"
@@ -339,14 +340,18 @@ template <class V, class I, int S, class Epi>
 cudaError_t launch_sellp_stream(const sb_sellp &A, const V *b, int64_t ldb, const Epi &epi,
                                 cudaStream_t st) {
     constexpr int VV = 16 / sizeof(V), VI = 16 / sizeof(I);
-    const int cap = (int)A.max_block_entries;
+    // stage capacity: the largest block if it fits 2048 entries, else chunks of 2048
+    // entries (whole columns) streamed through the ring
+    const int cap = (int)std::min<int64_t>(A.max_block_entries, std::max<int64_t>(2048 / S * S, S));
     const size_t cap_v = (size_t)cap + 2 * VV, cap_c = (size_t)cap + 2 * VI;
     const size_t off_c = (cap_v * sizeof(V) + 15) & ~size_t(15);
     const size_t stage = (off_c + cap_c * sizeof(I) + 15) & ~size_t(15);
-    auto kern = sellp_stream_kernel<V, I, S, Epi>;
+    // whole slice blocks when the largest fits a 2048-entry stage, else column chunks
+    auto kern = A.max_block_entries <= cap ? sellp_block_kernel<V, I, S, Epi> : sellp_chunk_kernel<V, I, S, Epi>;
     static int configured = 0;
     if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(sellp_block_kernel<V, I, S, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(sellp_chunk_kernel<V, I, S, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         configured = 1;
     }
     int grid = persistent_grid(kern, 128, 2 * stage);
@@ -362,7 +367,6 @@ template <class V, class I, class Epi>
 cudaError_t sellp_apply(const sb_sellp &A, const V *b, int64_t ldb, const Epi &epi, cudaStream_t st) {
     if (A.rows == 0) return cudaSuccess;
     const bool staged = A.max_block_entries > 0 &&
-                        2 * (size_t)A.max_block_entries * (sizeof(V) + sizeof(I)) <= 96 * 1024 &&
                         ((uintptr_t)A.values % 16 == 0) && ((uintptr_t)A.col_idxs % 16 == 0) &&
                         (A.slice_size == 32 || A.slice_size == 64 || A.slice_size == 128);
     if (staged) {
