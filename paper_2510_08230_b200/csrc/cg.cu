@@ -445,8 +445,16 @@ template <class V, class I>
 bool cg_persistent_launch(const sb_matrix &M, const CgPArgs &proto, cudaStream_t st, cudaError_t &err) {
     constexpr int R = 256;
     err = cudaSuccess;
-    if (M.format != SB_FMT_CSR) return false;
-    const sb_csr &A = *(const sb_csr *)M.mat;
+    sb_csr A;
+    if (M.format == SB_FMT_CSR) {
+        A = *(const sb_csr *)M.mat;
+    } else if (M.format == SB_FMT_COO) {  // row-pointer-indexed COO: the same CSR arrays
+        const sb_coo &C = *(const sb_coo *)M.mat;
+        if (!C.plan || !C.plan->row_ptrs || !C.plan->csr_plan) return false;
+        A = sb_csr{C.rows, C.cols, C.nnz, C.plan->row_ptrs, C.col_idxs, C.values, C.plan->csr_plan};
+    } else {
+        return false;
+    }
     if (!A.plan || A.plan->kernel != SB_CSR_STREAM || A.rows == 0) return false;
     const int cap = A.plan->block_rows == 256 ? A.plan->nnz_cap
                                               : (A.plan->block_rows == 128 ? A.plan->nnz_cap256 : 0);

@@ -364,3 +364,15 @@ def test_int64_indices_identical(dev, kind):
     for (l32, x32), (l64, x64) in zip(runs[:half], runs[half:]):
         assert l32.iterations == l64.iterations and l32.residual_history == l64.residual_history
         np.testing.assert_array_equal(x32, x64)
+
+
+def test_persistent_cg_on_indexed_coo(dev):
+    """Row-pointer-indexed COO runs the persistent CG like its CSR: same iterations."""
+    from paper_2510_08230_b200 import _lib
+    a = gen.stencil_csr(dev, 20, dim=3)
+    c = sp.coo_from_csr(a)
+    lc, xc, _ = solve(dev, "cg", c, np.ones(a.rows), [sp.Iteration(2000), sp.ResidualNorm(1e-8)])
+    assert int(_lib.fn("sb_cg_last_loop")()) == 3
+    la, xa, _ = solve(dev, "cg", a, np.ones(a.rows), [sp.Iteration(2000), sp.ResidualNorm(1e-8)])
+    assert lc.iterations == la.iterations and lc.residual_history == la.residual_history
+    np.testing.assert_array_equal(xc, xa)
