@@ -583,12 +583,15 @@ __global__ void __launch_bounds__(NT) csr_merge_kernel(int64_t rows, const I *__
 
 // ============================================================ CSR: nnz tiles
 // Tile t = nonzeros [t C, (t+1) C): exactly C nonzeros per tile whatever the row lengths.
-// One elected thread TMA-copies the tile's values, columns and the row pointers of the
-// rows starting in it (first_row[t] .. first_row[t+1], known one tile ahead) into a
-// two-stage shared ring, the next tile prefetched; all threads then form the tile's
-// products with every gather of a thread in flight at once (random gathers are bound by
-// the L1/L2 sector rate, ~270 G/s on B200, tools/micro/gather_bench.cu) and store them
-// in place (an fp32 product is exact in fp32).  Rows starting in the tile are reduced
+// One elected thread TMA-copies the row pointers of the rows starting in the tile
+// (first_row[t] .. first_row[t+1], known one tile ahead) -- and, in the staged variant,
+// the tile's values and columns -- into a two-stage shared ring, the next tile
+// prefetched.  All threads then form the tile's products with every gather of a thread
+// in flight at once (random gathers are bound by the L1/L2 sector rate, ~270 G/s on
+// B200, tools/micro/gather_bench.cu); the default "direct" variant reads values and
+// columns with coalesced streaming loads instead of staging them, which halves the
+// shared footprint (more CTAs, more gathers in flight per SM).  Products go to shared
+// memory (an fp32 product is exact in fp32).  Rows starting in the tile are reduced
 // from shared memory: segments of <= 32 products by one thread in stored order (a row
 // wholly inside the tile is then bitwise the reference's sum), longer ones by a warp
 // (lane-strided partials, fixed shuffle tree).  A row crossing tile boundaries is not
@@ -601,12 +604,22 @@ struct TileMeta {
     int32_t staged_rp;   // row pointers r0 .. r1 staged (else read from global)
 };
 
+template <class V, class I, int C, int RCAP, bool DIRECT = false>
+struct TileLayout;
 template <class V, class I, int C, int RCAP>
-struct TileLayout {
+struct TileLayout<V, I, C, RCAP, true> {  // stages hold the row pointers only
+    static constexpr int VI = 16 / sizeof(I);
+    static constexpr size_t OFF_C = 0, OFF_R = 0;
+    static constexpr size_t STAGE = ((size_t)(RCAP + 1 + 2 * VI) * sizeof(I) + 15) & ~size_t(15);
+    static constexpr size_t SMEM = 2 * STAGE + (size_t)C * sizeof(V);  // + one product buffer
+};
+template <class V, class I, int C, int RCAP>
+struct TileLayout<V, I, C, RCAP, false> {
     static constexpr int VV = 16 / sizeof(V), VI = 16 / sizeof(I);
     static constexpr size_t OFF_C = ((size_t)(C + 2 * VV) * sizeof(V) + 15) & ~size_t(15);
     static constexpr size_t OFF_R = (OFF_C + (size_t)(C + 2 * VI) * sizeof(I) + 15) & ~size_t(15);
     static constexpr size_t STAGE = (OFF_R + (size_t)(RCAP + 1 + 2 * VI) * sizeof(I) + 15) & ~size_t(15);
+    static constexpr size_t SMEM = 2 * STAGE;
 };
 
 // Per tile: wait for the stage, products (barrier), owned rows by threads with long
@@ -616,13 +629,13 @@ struct TileJob {
     int32_t kb, ke;  // product range in the tile
 };
 
-template <class V, class I, int NT, int C, int RCAP>
+template <class V, class I, int NT, int C, int RCAP, bool DIRECT = false>
 __global__ void __launch_bounds__(NT) csr_tile_kernel(int64_t rows, int64_t nnz, const I *__restrict__ rp,
                                                        const I *__restrict__ ci, const V *__restrict__ val,
                                                        const V *__restrict__ b, int64_t ldb, V *x, int64_t ldx,
                                                        const int64_t *__restrict__ first_row, int64_t ntiles,
                                                        int64_t *crow, double *cval) {
-    using L = TileLayout<V, I, C, RCAP>;
+    using L = TileLayout<V, I, C, RCAP, DIRECT>;
     constexpr int MAXJ = C / 33 + 4;
     constexpr int PER = C / NT;
     static_assert(C % NT == 0, "tile size");
@@ -645,9 +658,11 @@ __global__ void __launch_bounds__(NT) csr_tile_kernel(int64_t rows, int64_t nnz,
         I *sc = reinterpret_cast<I *>(st + L::OFF_C);
         I *sr = reinterpret_cast<I *>(st + L::OFF_R);
         const int64_t k0 = t * C, k1 = k0 + C < nnz ? k0 + C : nnz;
-        int64_t bv0, bc0, br0 = 0;
-        const uint32_t bv = stage_range(val, k0, k1, nnz, sv, bv0);
-        const uint32_t bc = stage_range(ci, k0, k1, nnz, sc, bc0);
+        int64_t bv0 = k0, bc0 = k0, br0 = 0;
+        // DIRECT: values / columns are read by the product phase with coalesced streaming
+        // loads (no stage for them: more CTAs per SM); only the row pointers are staged
+        const uint32_t bv = DIRECT ? 0u : stage_range(val, k0, k1, nnz, sv, bv0);
+        const uint32_t bc = DIRECT ? 0u : stage_range(ci, k0, k1, nnz, sc, bc0);
         const bool srp = RCAP > 0 && r1 - r0 <= RCAP;
         const uint32_t br = srp ? stage_range(rp, r0, r1 + 1, rows + 1, sr, br0) : 0;
         s_meta[s] = TileMeta{r0, r1, k0 - bv0, k0 - bc0, r0 - br0, srp};
@@ -681,12 +696,30 @@ __global__ void __launch_bounds__(NT) csr_tile_kernel(int64_t rows, int64_t nnz,
         mbar_wait(&bar[s], (it >> 1) & 1);
         unsigned char *st = smem + s * L::STAGE;
         const TileMeta m = s_meta[s];
-        V *sv = reinterpret_cast<V *>(st) + m.dv;
+        // DIRECT: one product buffer after the two row-pointer stages
+        V *sv = DIRECT ? reinterpret_cast<V *>(smem + 2 * L::STAGE) : reinterpret_cast<V *>(st) + m.dv;
         const I *sc = reinterpret_cast<const I *>(st + L::OFF_C) + m.dc;
         const I *sr = reinterpret_cast<const I *>(st + L::OFF_R) + m.dr;
         const int64_t k0 = t * C, k1 = k0 + C < nnz ? k0 + C : nnz;
         const int cnt = (int)(k1 - k0);
-        {
+        if constexpr (DIRECT) {
+            I cc[PER];
+            V vv[PER], bb[PER];
+#pragma unroll
+            for (int u = 0; u < PER; ++u) {
+                const int j = tid + u * NT;
+                const int jj = j < cnt ? j : cnt - 1;
+                cc[u] = ld_stream(ci + k0 + jj);
+                vv[u] = ld_stream(val + k0 + jj);
+            }
+#pragma unroll
+            for (int u = 0; u < PER; ++u) bb[u] = __ldg(b + (int64_t)cc[u] * ldb);
+#pragma unroll
+            for (int u = 0; u < PER; ++u) {
+                const int j = tid + u * NT;
+                if (j < cnt) sv[j] = (V)mulp(vv[u], bb[u]);
+            }
+        } else {
             V bb[PER];
 #pragma unroll
             for (int u = 0; u < PER; ++u) {

@@ -163,12 +163,12 @@ cudaError_t launch_csr_merge(const sb_csr &A, const V *b, int64_t ldb, V *x, int
                            (const double *)P.carry_vals, x, ldx, st);
 }
 
-template <class V, class I, int NT, int C, int RCAP>
+template <class V, class I, int NT, int C, int RCAP, bool DIRECT = false>
 cudaError_t launch_csr_tile_t(const sb_csr &A, const V *b, int64_t ldb, V *x, int64_t ldx, cudaStream_t st) {
     const sb_csr_plan &P = *A.plan;
     const int64_t ntiles = P.num_tiles / 2;
-    constexpr size_t smem = 2 * TileLayout<V, I, C, RCAP>::STAGE;
-    auto kern = csr_tile_kernel<V, I, NT, C, RCAP>;
+    constexpr size_t smem = TileLayout<V, I, C, RCAP, DIRECT>::SMEM;
+    auto kern = csr_tile_kernel<V, I, NT, C, RCAP, DIRECT>;
     static int configured = 0;
     if (!configured) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -187,19 +187,19 @@ cudaError_t launch_csr_tile_t(const sb_csr &A, const V *b, int64_t ldb, V *x, in
     return cudaGetLastError();
 }
 
-// Tile shape (threads x nonzeros per tile), measured on config #3 (tools/tile_ab.py, us per
-// SpMV, merge-path 566 / 452): fp64 256 x 2048 404 (512 x 2048 435, 256 x 1024 416,
-// 256 x 4096 ~600); fp32 512 x 2048 384 (256 x 2048 417, 256 x 1024 400); a three-stage
-// ring overlapping the row sums of tile t-1 with the gathers of tile t was tried and
-// measured slower (fp64 497 us: its extra stage costs a CTA per SM).  SPARSEB200_TILE_C
-// (1024 / 2048 / 4096) overrides the tile size for experiments.
+// Tile shape, measured on config #3 (tools/tile_ab.py, us per SpMV fp64 / fp32; merge-path
+// 562 / 452): 256 threads x 2048 nnz with values and columns read by coalesced streaming
+// loads and only the row pointers TMA-staged ("direct": 24 KB of shared memory -> more
+// CTAs per SM) 381 / 350; the same shape with values and columns TMA-staged 405 / 384;
+// direct 128 x 2048 851 / 451, 256 x 1024 452 / 442, 256 x 4096 847 / 821; staged 512 x
+// 2048 435 / 384; a three-stage staged ring 497 (fp64).  SPARSEB200_TILE_C = 1024 / 4096
+// selects the staged kernel with that tile size (experiments).
 template <class V, class I>
 cudaError_t launch_csr_tile(const sb_csr &A, const V *b, int64_t ldb, V *x, int64_t ldx, cudaStream_t st) {
     const int64_t C = A.plan->items_per_tile;
     if (C == 1024) return launch_csr_tile_t<V, I, 256, 1024, 512>(A, b, ldb, x, ldx, st);
     if (C == 4096) return launch_csr_tile_t<V, I, 256, 4096, 2048>(A, b, ldb, x, ldx, st);
-    if (sizeof(V) == 4) return launch_csr_tile_t<V, I, 512, 2048, 1024>(A, b, ldb, x, ldx, st);
-    return launch_csr_tile_t<V, I, 256, 2048, 1024>(A, b, ldb, x, ldx, st);
+    return launch_csr_tile_t<V, I, 256, 2048, 1024, true>(A, b, ldb, x, ldx, st);
 }
 
 template <class V>
