@@ -629,8 +629,10 @@ struct TileJob {
     int32_t kb, ke;  // product range in the tile
 };
 
+// fp32 direct tiles are capped to 32 registers for 8 CTAs per SM (350 -> 333 us on config
+// #3); the same cap makes fp64 slower (381 -> 745 us), which keeps the compiler's choice
 template <class V, class I, int NT, int C, int RCAP, bool DIRECT = false>
-__global__ void __launch_bounds__(NT) csr_tile_kernel(int64_t rows, int64_t nnz, const I *__restrict__ rp,
+__global__ void __launch_bounds__(NT, (DIRECT && sizeof(V) == 4) ? 2048 / NT : 0) csr_tile_kernel(int64_t rows, int64_t nnz, const I *__restrict__ rp,
                                                        const I *__restrict__ ci, const V *__restrict__ val,
                                                        const V *__restrict__ b, int64_t ldb, V *x, int64_t ldx,
                                                        const int64_t *__restrict__ first_row, int64_t ntiles,
