@@ -11,7 +11,7 @@ from paper_2510_08230_b200 import sparseops as sp  # noqa: E402
 from tools.sweep_configs import timed_spmv  # noqa: E402
 
 dev = sp.create_device("cuda", 0)
-flush = torch.zeros(32 * 1024 * 1024, dtype=torch.float64, device="cuda")
+flush = torch.zeros(128 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 1 GB
 for name, mk, fl in (("poisson3d_128", lambda pr: gen.poisson3d(dev, 128, precision=pr), None),
                      ("poisson2d_1000", lambda pr: gen.poisson2d(dev, 1000, precision=pr), flush)):
     for prec in (sp.Precision.single, sp.Precision.double):
