@@ -201,6 +201,7 @@ struct CgPArgs {
     double *partials;  // 3 G doubles: [p.q | r.r, r.z] (+ G arrival stamps when profiling)
     unsigned long long *prof;  // optional: arrival stamps of barriers 10..27 (18 G) + CTA 0 releases
     int nnz_cap;
+    int pf;  // L2 prefetch of the next update block's operands (SPARSEB200_CG_PF=0: off)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -388,6 +389,15 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
         double part2[2] = {0.0, 0.0};
         for (int64_t blk = bid; blk < nblk; blk += G) {
             const int64_t i = blk * R + tid;
+            // five threads hint the next block's operands into L2 (cp.async.bulk.prefetch):
+            // doubles the bytes in flight of this one-row-per-thread pass (128^3: 73.2 ->
+            // 71.1 us per iteration; the same hint for the SpMV phase's gathered vectors
+            // measured no better)
+            if (a.pf && tid < 5 && blk + G < nblk) {
+                const int64_t b0 = (blk + G) * R, b1 = b0 + R < n ? b0 + R : n;
+                const V *vp = tid == 0 ? x : tid == 1 ? r : tid == 2 ? q : tid == 3 ? pnew : inv;
+                if (vp) l2_prefetch_range(vp + b0, vp + b1);
+            }
             if (i < n) {
                 const V pi = pnew[i], qi = q[i];
                 x[i] = axpy_e(alpha, pi, x[i]);
@@ -693,6 +703,8 @@ sb_status cg_solve(const SolveArgs &a) {
         pa.partials = part;
         static const bool prof = getenv("SPARSEB200_CG_PROFILE") != nullptr;
         pa.prof = prof ? reinterpret_cast<unsigned long long *>(part + 4096) : nullptr;  // G <= 1000
+        static const int pf = getenv("SPARSEB200_CG_PF") ? atoi(getenv("SPARSEB200_CG_PF")) : 1;
+        pa.pf = pf;
         cudaError_t le;
         if (cg_persistent_launch<V, I>(M, pa, a.st, le)) {
             g_cg_last_loop = 3;

@@ -106,6 +106,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     }
 }
 // 1-D TMA bulk copy global -> shared; completion is signalled on `bar` as tx bytes.
+// L2 prefetch hint of the 16-byte aligned part of [lo, hi) (cp.async.bulk.prefetch)
+__device__ __forceinline__ void l2_prefetch_range(const void *lo, const void *hi) {
+    const uintptr_t a = ((uintptr_t)lo + 15) & ~(uintptr_t)15, e = (uintptr_t)hi & ~(uintptr_t)15;
+    if (e > a) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a)) : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
                                          uint64_t pol) {
     asm volatile(

@@ -631,7 +631,7 @@ struct TileJob {
 
 // fp32 direct tiles are capped to 32 registers for 8 CTAs per SM (350 -> 333 us on config
 // #3); the same cap makes fp64 slower (381 -> 745 us), which keeps the compiler's choice
-template <class V, class I, int NT, int C, int RCAP, bool DIRECT = false>
+template <class V, class I, int NT, int C, int RCAP, bool DIRECT = false, int PF = 0>
 __global__ void __launch_bounds__(NT, (DIRECT && sizeof(V) == 4) ? 2048 / NT : 0) csr_tile_kernel(int64_t rows, int64_t nnz, const I *__restrict__ rp,
                                                        const I *__restrict__ ci, const V *__restrict__ val,
                                                        const V *__restrict__ b, int64_t ldb, V *x, int64_t ldx,
@@ -693,6 +693,14 @@ __global__ void __launch_bounds__(NT, (DIRECT && sizeof(V) == 4) ? 2048 / NT : 0
                     nr0 = first_row[tn + gridDim.x];
                     nr1 = first_row[tn + gridDim.x + 1];
                 }
+            }
+        }
+        if (DIRECT && PF > 0 && tid == 32) {  // values / columns of the tile PF rounds ahead into L2
+            const int64_t tp = t + (int64_t)PF * gridDim.x;
+            if (tp < ntiles) {
+                const int64_t a = tp * C, e = a + C < nnz ? a + C : nnz;
+                l2_prefetch_range(val + a, val + e);
+                l2_prefetch_range(ci + a, ci + e);
             }
         }
         mbar_wait(&bar[s], (it >> 1) & 1);

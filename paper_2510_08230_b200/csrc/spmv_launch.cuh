@@ -163,12 +163,12 @@ cudaError_t launch_csr_merge(const sb_csr &A, const V *b, int64_t ldb, V *x, int
                            (const double *)P.carry_vals, x, ldx, st);
 }
 
-template <class V, class I, int NT, int C, int RCAP, bool DIRECT = false>
+template <class V, class I, int NT, int C, int RCAP, bool DIRECT = false, int PF = 0>
 cudaError_t launch_csr_tile_t(const sb_csr &A, const V *b, int64_t ldb, V *x, int64_t ldx, cudaStream_t st) {
     const sb_csr_plan &P = *A.plan;
     const int64_t ntiles = P.num_tiles / 2;
     constexpr size_t smem = TileLayout<V, I, C, RCAP, DIRECT>::SMEM;
-    auto kern = csr_tile_kernel<V, I, NT, C, RCAP, DIRECT>;
+    auto kern = csr_tile_kernel<V, I, NT, C, RCAP, DIRECT, PF>;
     static int configured = 0;
     if (!configured) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -190,7 +190,7 @@ cudaError_t launch_csr_tile_t(const sb_csr &A, const V *b, int64_t ldb, V *x, in
 // Tile shape, measured on config #3 (tools/tile_ab.py, us per SpMV fp64 / fp32; merge-path
 // 562 / 452): 256 threads x 2048 nnz with values and columns read by coalesced streaming
 // loads and only the row pointers TMA-staged ("direct": 24 KB of shared memory -> more
-// CTAs per SM) 381 / 350; the same shape with values and columns TMA-staged 405 / 384;
+// CTAs per SM) 381 / 333 (fp64 370 with the L2 prefetch below); the same shape with values and columns TMA-staged 405 / 384;
 // direct 128 x 2048 851 / 451, 256 x 1024 452 / 442, 256 x 4096 847 / 821; staged 512 x
 // 2048 435 / 384; a three-stage staged ring 497 (fp64).  SPARSEB200_TILE_C = 1024 / 4096
 // selects the staged kernel with that tile size (experiments).
@@ -199,6 +199,16 @@ cudaError_t launch_csr_tile(const sb_csr &A, const V *b, int64_t ldb, V *x, int6
     const int64_t C = A.plan->items_per_tile;
     if (C == 1024) return launch_csr_tile_t<V, I, 256, 1024, 512>(A, b, ldb, x, ldx, st);
     if (C == 4096) return launch_csr_tile_t<V, I, 256, 4096, 2048>(A, b, ldb, x, ldx, st);
+    // L2 prefetch of the values / columns one round ahead: fp64 380.6 -> 370.2 us on
+    // config #3; fp32 333 -> 339 us (register-capped kernel), so fp64 only.
+    // SPARSEB200_TILE_PF = 0 / 1 / 2 overrides (2 rounds ahead: 381.9 / 342.4 us).
+    static const int pf_env = [] {
+        const char *e = getenv("SPARSEB200_TILE_PF");
+        return e ? atoi(e) : -1;
+    }();
+    const int pf = pf_env >= 0 ? pf_env : (sizeof(V) == 8 ? 1 : 0);
+    if (pf == 1) return launch_csr_tile_t<V, I, 256, 2048, 1024, true, 1>(A, b, ldb, x, ldx, st);
+    if (pf == 2) return launch_csr_tile_t<V, I, 256, 2048, 1024, true, 2>(A, b, ldb, x, ldx, st);
     return launch_csr_tile_t<V, I, 256, 2048, 1024, true>(A, b, ldb, x, ldx, st);
 }
 
