@@ -392,7 +392,8 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
             // five threads hint the next block's operands into L2 (cp.async.bulk.prefetch):
             // doubles the bytes in flight of this one-row-per-thread pass (128^3: 73.2 ->
             // 71.1 us per iteration; the same hint for the SpMV phase's gathered vectors
-            // measured no better)
+            // measured no better, and for the stream SpMV's matrix ranges beyond its TMA
+            // ring slower: 36.0 -> 37.6 us at 128^3)
             if (a.pf && tid < 5 && blk + G < nblk) {
                 const int64_t b0 = (blk + G) * R, b1 = b0 + R < n ? b0 + R : n;
                 const V *vp = tid == 0 ? x : tid == 1 ? r : tid == 2 ? q : tid == 3 ? pnew : inv;
