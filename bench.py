@@ -282,7 +282,7 @@ def run_ours(args):
         achieved = cg_iter_bytes / (cg_iter_ms / 1e3) / 1e9
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": _persistent_traffic(cg_iter_bytes),
-                    "kernel": "cg_persistent_kernel<double,int,256>",
+                    "kernel": f"cg_persistent_kernel<double,int,{int(_lib.fn('sb_cg_last_block_rows')())}>",
                     "alg_bytes_per_launch": cg_iter_bytes * log.iterations,
                     "launch_us": ms / args.steps * 1e3, "peak_source": spmv_roof["peak_source"],
                     "note": "bytes per launch = iterations x (matrix + 12 vector passes); "

@@ -208,6 +208,9 @@ void sb_set_cg_fused(int mode);
 /* Loop shape used by this thread's last CG solve: 0 three-kernel graph loop, 1 fused-
    direction graph loop, 3 persistent cooperative kernel (one launch per solve). */
 int sb_cg_last_loop(void);
+/* Rows per block (= threads per CTA) of this thread's last persistent CG solve (512 or
+   256; 0 if the last solve ran a graph loop). */
+int sb_cg_last_block_rows(void);
 
 #define SB_VALUE_DECLS(VN)                                                                       \
     /* core.dot / norm2 / axpy / scal / copy_into (core.py:358-401); jacobi apply (precond.py:57-63) */ \

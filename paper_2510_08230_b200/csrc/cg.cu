@@ -449,12 +449,13 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
     }
 }
 
-// Launch the persistent loop if the matrix is a stream-kernel CSR whose 256-row block
+// Launch the persistent loop if the matrix is a stream-kernel CSR whose R-row block
 // stage fits, and the grid can be co-resident (cooperative launch); false = not
 // applicable (the caller runs the graph loop).
-template <class V, class I>
-bool cg_persistent_launch(const sb_matrix &M, const CgPArgs &proto, cudaStream_t st, cudaError_t &err) {
-    constexpr int R = 256;
+static thread_local int g_cg_last_rows = 0;  // block rows of the last persistent launch
+
+template <class V, class I, int R>
+bool cg_persistent_launch_r(const sb_matrix &M, const CgPArgs &proto, cudaStream_t st, cudaError_t &err) {
     err = cudaSuccess;
     sb_csr A;
     if (M.format == SB_FMT_CSR) {
@@ -467,9 +468,10 @@ bool cg_persistent_launch(const sb_matrix &M, const CgPArgs &proto, cudaStream_t
         return false;
     }
     if (!A.plan || A.plan->kernel != SB_CSR_STREAM || A.rows == 0) return false;
-    const int cap = A.plan->block_rows == 256 ? A.plan->nnz_cap
-                                              : (A.plan->block_rows == 128 ? A.plan->nnz_cap256 : 0);
+    int cap = A.plan->block_rows == 256 ? A.plan->nnz_cap
+                                        : (A.plan->block_rows == 128 ? A.plan->nnz_cap256 : 0);
     if (cap <= 0) return false;
+    cap *= R / 256;  // a block of R rows holds at most R / 256 times a 256-row block's cap
     const size_t smem = 2 * StreamLayout<V, I>(R, cap).stage_bytes();
     if (smem > 200 * 1024) return false;
     auto kern = cg_persistent_kernel<V, I, R>;
@@ -500,7 +502,23 @@ bool cg_persistent_launch(const sb_matrix &M, const CgPArgs &proto, cudaStream_t
         cudaGetLastError();
         return false;  // not co-resident here: graph loop instead
     }
+    g_cg_last_rows = R;
     return true;
+}
+
+template <class V, class I>
+bool cg_persistent_launch(const sb_matrix &M, const CgPArgs &proto, cudaStream_t st, cudaError_t &err) {
+    // Small systems (<= 2^20 rows): 512-row blocks (2 CTAs of 512 threads per SM: half the
+    // barrier arrivals) where their stage fits; else 256 (cg_modes.py, us per iteration,
+    // 256 -> 512 rows: 64^3 15.6 -> 14.5-14.8, 96^3 32.8 -> 32.0-32.3; 128^3 72.2 ->
+    // 72.2-72.4 and bench.py 13.80k -> 13.62-13.74k iterations/s).  SPARSEB200_CG_R = 256 /
+    // 512 forces one.
+    static const int r_env = getenv("SPARSEB200_CG_R") ? atoi(getenv("SPARSEB200_CG_R")) : 0;
+    const int64_t rows = M.format == SB_FMT_CSR ? ((const sb_csr *)M.mat)->rows
+                                                : (M.format == SB_FMT_COO ? ((const sb_coo *)M.mat)->rows : 0);
+    const int r = r_env ? r_env : (rows <= (int64_t(1) << 20) ? 512 : 256);
+    if (r == 512 && cg_persistent_launch_r<V, I, 512>(M, proto, st, err)) return true;
+    return cg_persistent_launch_r<V, I, 256>(M, proto, st, err);
 }
 
 // CG loop shape: 3 = persistent kernel where applicable (default), else the graph loop
@@ -784,6 +802,7 @@ extern "C" {
 
 void sb_set_cg_fused(int mode) { g_cg_mode = mode; }
 int sb_cg_last_loop(void) { return g_cg_last_loop; }
+int sb_cg_last_block_rows(void) { return g_cg_last_loop == 3 ? g_cg_last_rows : 0; }
 
 #define SB_DEFS(V, VN, I, IN) \
     sb_status sb_cg_solve_##VN##_##IN(const sb_matrix *a, const void *inv_diag,                    \

@@ -373,6 +373,7 @@ def test_persistent_cg_on_indexed_coo(dev):
     c = sp.coo_from_csr(a)
     lc, xc, _ = solve(dev, "cg", c, np.ones(a.rows), [sp.Iteration(2000), sp.ResidualNorm(1e-8)])
     assert int(_lib.fn("sb_cg_last_loop")()) == 3
+    assert int(_lib.fn("sb_cg_last_block_rows")()) == 512  # small system, stencil stage fits
     la, xa, _ = solve(dev, "cg", a, np.ones(a.rows), [sp.Iteration(2000), sp.ResidualNorm(1e-8)])
     assert lc.iterations == la.iterations and lc.residual_history == la.residual_history
     np.testing.assert_array_equal(xc, xa)
