@@ -16,6 +16,8 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdlib>
+#include <type_traits>
 
 #include "capi_util.cuh"
 #include "solver_common.cuh"
@@ -61,11 +63,11 @@ __device__ __forceinline__ void wait_ready(const int *ready, int64_t j) {
     }
 }
 
-// Claims the next 32 rows (in solve order) for the calling warp; all lanes return the
-// same base.  Must be called by the full warp.
-__device__ __forceinline__ int64_t claim_rows(unsigned long long *counter) {
+// Claims the next 32 * k rows (in solve order) for the calling warp; all lanes return
+// the same base.  Must be called by the full warp.
+__device__ __forceinline__ int64_t claim_rows(unsigned long long *counter, unsigned k = 1) {
     unsigned long long base = 0;
-    if ((threadIdx.x & 31) == 0) base = atomicAdd(counter, 32ull);
+    if ((threadIdx.x & 31) == 0) base = atomicAdd(counter, 32ull * k);
     return (int64_t)__shfl_sync(0xffffffffu, base, 0);
 }
 
@@ -79,17 +81,24 @@ __device__ __forceinline__ bool tri_skip(const Ctl *c, int mode) {
     return false;
 }
 
-// x = T^{-1} b for a triangular CSR T whose structure was validated (tri_check_kernel)
-template <class V, class I, bool LOWER>
+// x = T^{-1} b for a triangular CSR T whose structure was validated (tri_check_kernel).
+// A warp claims RPT * 32 rows; lane l solves rows base + 32 u + l for u = 0 .. RPT-1 in
+// order.  Still deadlock-free: the lowest unsolved row has every dependency solved, and
+// its lane has finished all of its earlier rows, so it is the row that lane is on.  More
+// rows per claim = more of the sweep resident at once: the sweep is a pipeline whose
+// throughput is (rows in flight) / (hops per row's dependency chain).
+template <class V, class I, bool LOWER, int RPT = 1>
 __global__ void __launch_bounds__(256) sptrsv_kernel(int64_t n, const I *__restrict__ rp,
                                                      const I *__restrict__ ci, const V *__restrict__ val,
                                                      const V *b, int64_t ldb, V *x, int64_t ldx, int unit,
                                                      TriWs w, const Ctl *ctl, int skip_mode) {
     if (tri_skip(ctl, skip_mode)) return;
     for (;;) {
-        const int64_t base = claim_rows(w.counter);
+        const int64_t base = claim_rows(w.counter, RPT);
         if (base >= n) return;
-        const int64_t t = base + (threadIdx.x & 31);
+#pragma unroll 1
+        for (int u = 0; u < RPT; ++u) {
+        const int64_t t = base + 32 * u + (threadIdx.x & 31);
         if (t < n) {
             const int64_t i = LOWER ? t : n - 1 - t;
             double acc = (double)b[i * ldb] + 0.0;
@@ -105,6 +114,72 @@ __global__ void __launch_bounds__(256) sptrsv_kernel(int64_t n, const I *__restr
             }
             x[i * ldx] = (LOWER && unit) ? (V)acc : (V)__ddiv_rn(acc, diag);
             st_release_i32(w.ready + i, 1);
+        }
+        }
+    }
+}
+
+// Converged-polling variant: a warp claims RPT * 32 rows; every lane keeps a cursor into
+// its current row and, each round, consumes entries while their dependencies are ready
+// (never blocking inside divergent code, so no reliance on independent-thread scheduling
+// between lanes of one warp), publishes finished rows and moves on; a round in which no
+// lane of the warp progressed ends with a short sleep.  Same per-row arithmetic and order.
+template <class V, class I, bool LOWER, int RPT>
+__global__ void __launch_bounds__(256) sptrsv_poll_kernel(int64_t n, const I *__restrict__ rp,
+                                                          const I *__restrict__ ci, const V *__restrict__ val,
+                                                          const V *b, int64_t ldb, V *x, int64_t ldx, int unit,
+                                                          TriWs w, const Ctl *ctl, int skip_mode) {
+    if (tri_skip(ctl, skip_mode)) return;
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        const int64_t base = claim_rows(w.counter, RPT);
+        if (base >= n) return;
+        int u = -1;
+        int64_t i = 0, k = 0, ke = 0;
+        double acc = 0.0, diag = 1.0;
+        auto next_row = [&]() {
+            for (++u; u < RPT; ++u) {
+                const int64_t t = base + 32 * u + lane;
+                if (t >= n) {
+                    u = RPT;
+                    return;
+                }
+                i = LOWER ? t : n - 1 - t;
+                k = rp[i];
+                ke = rp[i + 1];
+                acc = (double)b[i * ldb] + 0.0;
+                diag = 1.0;
+                return;
+            }
+        };
+        next_row();
+        unsigned ns = 32;
+        while (__any_sync(0xffffffffu, u < RPT)) {
+            bool moved = false;
+            if (u < RPT) {
+                for (; k < ke; ++k) {
+                    const int64_t j = ci[k];
+                    if (LOWER ? j < i : j > i) {
+                        if (ld_acquire_i32(w.ready + j) == 0) break;
+                        acc = __dsub_rn(acc, mulp(val[k], __ldcg(x + j * ldx)));
+                    } else if (j == i) {
+                        diag = (double)val[k];
+                    }
+                    moved = true;
+                }
+                if (k == ke) {
+                    x[i * ldx] = (LOWER && unit) ? (V)acc : (V)__ddiv_rn(acc, diag);
+                    st_release_i32(w.ready + i, 1);
+                    next_row();
+                    moved = true;
+                }
+            }
+            if (__any_sync(0xffffffffu, moved)) {
+                ns = 32;
+            } else {
+                __nanosleep(ns);
+                if (ns < 256) ns <<= 1;
+            }
         }
     }
 }
@@ -149,15 +224,41 @@ cudaError_t launch_trsv(const sb_csr &T, bool lower, bool unit, const V *b, int6
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(w.counter, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
+    // Default: the converged-polling kernel, one row per lane (tools/precond_bench.py, IC-CG
+    // ms, blocking-spin -> polling: 64^3 98 -> 84, 96^3 341 -> 284, 128^3 1058 -> 867;
+    // ILU-GMRES conv-diff 64^3 137 -> 118).  SPARSEB200_TRSV_MODE=0 selects the blocking
+    // spin kernel; SPARSEB200_TRSV_RPT = 2 / 4 rows per lane (experimental: 128^3 IC-CG 588 /
+    // 430 ms, but 96^3 ~10x slower and 64^3 at 4 rows ~8x slower -- not a safe default).
+    static const int rpt = getenv("SPARSEB200_TRSV_RPT") ? atoi(getenv("SPARSEB200_TRSV_RPT")) : 1;
+    static const int mode = getenv("SPARSEB200_TRSV_MODE") ? atoi(getenv("SPARSEB200_TRSV_MODE")) : 1;
     const int grid = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)device_info().sms * 8);
-    if (lower)
-        sptrsv_kernel<V, I, true><<<grid, 256, 0, st>>>(n, (const I *)T.row_ptrs, (const I *)T.col_idxs,
-                                                        (const V *)T.values, b, ldb, x, ldx, unit ? 1 : 0, w,
-                                                        ctl, skip_mode);
-    else
-        sptrsv_kernel<V, I, false><<<grid, 256, 0, st>>>(n, (const I *)T.row_ptrs, (const I *)T.col_idxs,
-                                                         (const V *)T.values, b, ldb, x, ldx, 0, w, ctl,
-                                                         skip_mode);
+    auto go = [&](auto lower_c, auto rpt_c) {
+        if (mode == 1)
+            sptrsv_poll_kernel<V, I, decltype(lower_c)::value, decltype(rpt_c)::value><<<grid, 256, 0, st>>>(
+                n, (const I *)T.row_ptrs, (const I *)T.col_idxs, (const V *)T.values, b, ldb, x, ldx,
+                (lower && unit) ? 1 : 0, w, ctl, skip_mode);
+        else
+            sptrsv_kernel<V, I, decltype(lower_c)::value, decltype(rpt_c)::value><<<grid, 256, 0, st>>>(
+                n, (const I *)T.row_ptrs, (const I *)T.col_idxs, (const V *)T.values, b, ldb, x, ldx,
+                (lower && unit) ? 1 : 0, w, ctl, skip_mode);
+    };
+    using T_ = std::true_type;
+    using F_ = std::false_type;
+    using R1 = std::integral_constant<int, 1>;
+    using R2 = std::integral_constant<int, 2>;
+    using R4 = std::integral_constant<int, 4>;
+    using R8 = std::integral_constant<int, 8>;
+    if (lower) {
+        if (rpt == 8) go(T_{}, R8{});
+        else if (rpt == 4) go(T_{}, R4{});
+        else if (rpt == 2) go(T_{}, R2{});
+        else go(T_{}, R1{});
+    } else {
+        if (rpt == 8) go(F_{}, R8{});
+        else if (rpt == 4) go(F_{}, R4{});
+        else if (rpt == 2) go(F_{}, R2{});
+        else go(F_{}, R1{});
+    }
     return cudaGetLastError();
 }
 
