@@ -51,6 +51,39 @@ __device__ __forceinline__ int ld_acquire_i32(const int *p) {
 __device__ __forceinline__ void st_release_i32(int *p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// Value-as-flag publication (sptrsv_poll_kernel<..., VF = true>): x is pre-filled with a
+// signalling-NaN sentinel that floating-point arithmetic never produces (any NaN result
+// is a quiet NaN), the solved value is published with a release store and consumed with
+// one acquire load -- one L2 round trip per dependency instead of flag + value.
+template <class V>
+struct TriSentinel;
+template <>
+struct TriSentinel<double> {
+    static constexpr unsigned long long bits = 0x7FF4A5A5A5A5A5A5ull;
+};
+template <>
+struct TriSentinel<float> {
+    static constexpr unsigned bits = 0x7FA5A5A5u;
+};
+__device__ __forceinline__ bool ld_acquire_val(const double *p, double &v) {
+    unsigned long long u;
+    asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(u) : "l"(p) : "memory");
+    v = __longlong_as_double((long long)u);
+    return u != TriSentinel<double>::bits;
+}
+__device__ __forceinline__ bool ld_acquire_val(const float *p, float &v) {
+    unsigned u;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(u) : "l"(p) : "memory");
+    v = __uint_as_float(u);
+    return u != TriSentinel<float>::bits;
+}
+__device__ __forceinline__ void st_release_val(double *p, double v) {
+    asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"((unsigned long long)__double_as_longlong(v))
+                 : "memory");
+}
+__device__ __forceinline__ void st_release_val(float *p, float v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(__float_as_uint(v)) : "memory");
+}
 // Spin with a short back-off: hundreds of thousands of waiting threads issuing
 // back-to-back acquire loads would flood L2 and slow the very stores they wait for
 // (128^3 IC-CG: 1283 -> 1055 ms).  A level-sorted sweep order was also measured: it
@@ -79,6 +112,17 @@ __device__ __forceinline__ bool tri_skip(const Ctl *c, int mode) {
     if (mode == TRI_SKIP_CYCLE_END) return c->cycle_end != 0;
     if (mode == TRI_SKIP_UNLESS_CYCLE_END) return c->cycle_end == 0;
     return false;
+}
+
+template <class V>
+__global__ void tri_sentinel_fill_kernel(int64_t n, V *x, int64_t ldx, const Ctl *ctl, int skip_mode) {
+    if (tri_skip(ctl, skip_mode)) return;  // a skipped sweep leaves x untouched
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if constexpr (sizeof(V) == 8)
+            reinterpret_cast<unsigned long long *>(x)[i * ldx] = TriSentinel<double>::bits;
+        else
+            reinterpret_cast<unsigned *>(x)[i * ldx] = TriSentinel<float>::bits;
+    }
 }
 
 // x = T^{-1} b for a triangular CSR T whose structure was validated (tri_check_kernel).
@@ -124,7 +168,7 @@ __global__ void __launch_bounds__(256) sptrsv_kernel(int64_t n, const I *__restr
 // (never blocking inside divergent code, so no reliance on independent-thread scheduling
 // between lanes of one warp), publishes finished rows and moves on; a round in which no
 // lane of the warp progressed ends with a short sleep.  Same per-row arithmetic and order.
-template <class V, class I, bool LOWER, int RPT>
+template <class V, class I, bool LOWER, int RPT, bool VF = false>
 __global__ void __launch_bounds__(256) sptrsv_poll_kernel(int64_t n, const I *__restrict__ rp,
                                                           const I *__restrict__ ci, const V *__restrict__ val,
                                                           const V *b, int64_t ldb, V *x, int64_t ldx, int unit,
@@ -160,16 +204,27 @@ __global__ void __launch_bounds__(256) sptrsv_poll_kernel(int64_t n, const I *__
                 for (; k < ke; ++k) {
                     const int64_t j = ci[k];
                     if (LOWER ? j < i : j > i) {
-                        if (ld_acquire_i32(w.ready + j) == 0) break;
-                        acc = __dsub_rn(acc, mulp(val[k], __ldcg(x + j * ldx)));
+                        V xj;
+                        if constexpr (VF) {
+                            if (!ld_acquire_val(x + j * ldx, xj)) break;
+                        } else {
+                            if (ld_acquire_i32(w.ready + j) == 0) break;
+                            xj = __ldcg(x + j * ldx);
+                        }
+                        acc = __dsub_rn(acc, mulp(val[k], xj));
                     } else if (j == i) {
                         diag = (double)val[k];
                     }
                     moved = true;
                 }
                 if (k == ke) {
-                    x[i * ldx] = (LOWER && unit) ? (V)acc : (V)__ddiv_rn(acc, diag);
-                    st_release_i32(w.ready + i, 1);
+                    const V xi = (LOWER && unit) ? (V)acc : (V)__ddiv_rn(acc, diag);
+                    if constexpr (VF) {
+                        st_release_val(x + i * ldx, xi);
+                    } else {
+                        x[i * ldx] = xi;
+                        st_release_i32(w.ready + i, 1);
+                    }
                     next_row();
                     moved = true;
                 }
@@ -220,9 +275,7 @@ cudaError_t launch_trsv(const sb_csr &T, bool lower, bool unit, const V *b, int6
                         const TriWs &w, const Ctl *ctl, int skip_mode, cudaStream_t st) {
     const int64_t n = T.rows;
     if (n == 0) return cudaSuccess;
-    cudaError_t e = cudaMemsetAsync(w.ready, 0, sizeof(int) * (size_t)n, st);
-    if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(w.counter, 0, sizeof(unsigned long long), st);
+    cudaError_t e = cudaMemsetAsync(w.counter, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
     // Default: the converged-polling kernel, one row per lane (tools/precond_bench.py, IC-CG
     // ms, blocking-spin -> polling: 64^3 98 -> 84, 96^3 341 -> 284, 128^3 1058 -> 867;
@@ -230,10 +283,30 @@ cudaError_t launch_trsv(const sb_csr &T, bool lower, bool unit, const V *b, int6
     // spin kernel; SPARSEB200_TRSV_RPT = 2 / 4 rows per lane (experimental: 128^3 IC-CG 588 /
     // 430 ms, but 96^3 ~10x slower and 64^3 at 4 rows ~8x slower -- not a safe default).
     static const int rpt = getenv("SPARSEB200_TRSV_RPT") ? atoi(getenv("SPARSEB200_TRSV_RPT")) : 1;
-    static const int mode = getenv("SPARSEB200_TRSV_MODE") ? atoi(getenv("SPARSEB200_TRSV_MODE")) : 1;
+    // Mode 2 (default): polling with the value as its own flag (IC-CG 128^3 866 -> 804 ms,
+    // 96^3 282 -> 261, 64^3 84 -> 78; ILU-GMRES 64^3 118 -> 109); 1: polling with separate
+    // ready flags (also used when x overlaps b); 0: blocking spin.
+    static const int mode = getenv("SPARSEB200_TRSV_MODE") ? atoi(getenv("SPARSEB200_TRSV_MODE")) : 2;
     const int grid = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)device_info().sms * 8);
+    // value-as-flag needs x disjoint from b (the sentinel fill would clobber b)
+    const char *xb = (const char *)x, *bb = (const char *)b;
+    const size_t span = (size_t)((n - 1) * ldx + 1) * sizeof(V);
+    const size_t bspan = (size_t)((n - 1) * ldb + 1) * sizeof(V);
+    const bool disjoint = xb + span <= bb || bb + bspan <= xb;
+    const bool vf = mode == 2 && disjoint;
+    if (!vf) {
+        e = cudaMemsetAsync(w.ready, 0, sizeof(int) * (size_t)n, st);
+        if (e != cudaSuccess) return e;
+    } else {
+        tri_sentinel_fill_kernel<V><<<(int)std::min<int64_t>(ceil_div(n, 256), (int64_t)device_info().sms * 16), 256, 0, st>>>(
+            n, x, ldx, ctl, skip_mode);
+    }
     auto go = [&](auto lower_c, auto rpt_c) {
-        if (mode == 1)
+        if (vf)
+            sptrsv_poll_kernel<V, I, decltype(lower_c)::value, decltype(rpt_c)::value, true><<<grid, 256, 0, st>>>(
+                n, (const I *)T.row_ptrs, (const I *)T.col_idxs, (const V *)T.values, b, ldb, x, ldx,
+                (lower && unit) ? 1 : 0, w, ctl, skip_mode);
+        else if (mode >= 1)
             sptrsv_poll_kernel<V, I, decltype(lower_c)::value, decltype(rpt_c)::value><<<grid, 256, 0, st>>>(
                 n, (const I *)T.row_ptrs, (const I *)T.col_idxs, (const V *)T.values, b, ldb, x, ldx,
                 (lower && unit) ? 1 : 0, w, ctl, skip_mode);

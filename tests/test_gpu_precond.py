@@ -54,7 +54,7 @@ def test_factorizations_bitwise(dev, vdt):
 
 def test_trisolve_large_bitwise(dev):
     """Sweeps over 3-D Poisson 48^3 factors (110k rows, deep dependency chains) equal the
-    oracle's sequential loops bit for bit; lower, unit lower, upper."""
+    oracle's sequential loops bit for bit; lower, unit lower, upper, in place, fp32."""
     a = gen.stencil_csr(dev, 48, dim=3)
     rp, ci, v = _arrays(a)
     f = sp.ilu0_factorize(a)
@@ -75,6 +75,21 @@ def test_trisolve_large_bitwise(dev):
     x = out(dev, a.rows, np.float64)
     sp.solve_lower_tri(g.l, vec(dev, bv), x)
     np.testing.assert_array_equal(host(x), sbref.trsv(gp, gc, gv, bv, lower=True)[2])
+    # in place (x is b): the value-as-flag sweep must fall back to separate ready flags
+    for mat, lower, unit, ref in ((f.l, True, True, (lp, lc, lv)), (f.u, False, False, (up, uc, uv))):
+        xb = vec(dev, bv)
+        (sp.solve_lower_tri(mat, xb, xb, unit_diag=True) if lower else sp.solve_upper_tri(mat, xb, xb))
+        np.testing.assert_array_equal(host(xb), sbref.trsv(*ref, bv, lower=lower, unit_diag=unit)[2])
+    # fp32 factors: the 32-bit sentinel path
+    a32 = gen.stencil_csr(dev, 24, dim=3, precision=sp.Precision.single)
+    rp, ci, v = _arrays(a32)
+    f32 = sp.ilu0_factorize(a32)
+    _, fv = sbref.ilu0(rp, ci, v)
+    (lp, lc, lv), (up, uc, uv) = sbref.split_lu(rp, ci, fv)
+    b32 = np.random.default_rng(4).standard_normal(a32.rows).astype(np.float32)
+    x = out(dev, a32.rows, np.float32)
+    sp.solve_upper_tri(f32.u, vec(dev, b32), x)
+    np.testing.assert_array_equal(host(x), sbref.trsv(up, uc, uv, b32, lower=False)[2])
 
 
 def test_error_kinds_and_rows(dev):
