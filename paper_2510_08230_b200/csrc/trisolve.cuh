@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(256) sptrsv_kernel(int64_t n, const I *__restr
 }
 
 // Converged-polling variant: a warp claims RPT * 32 rows; every lane keeps a cursor into
-// its current row and, each round, consumes entries while their dependencies are ready
+// each of its rows and, each round, consumes entries while their dependencies are ready
 // (never blocking inside divergent code, so no reliance on independent-thread scheduling
 // between lanes of one warp), publishes finished rows and moves on; a round in which no
 // lane of the warp progressed ends with a short sleep.  Same per-row arithmetic and order.
@@ -178,32 +178,35 @@ __global__ void __launch_bounds__(256) sptrsv_poll_kernel(int64_t n, const I *__
     for (;;) {
         const int64_t base = claim_rows(w.counter, RPT);
         if (base >= n) return;
-        int u = -1;
-        int64_t i = 0, k = 0, ke = 0;
-        double acc = 0.0, diag = 1.0;
-        auto next_row = [&]() {
-            for (++u; u < RPT; ++u) {
-                const int64_t t = base + 32 * u + lane;
-                if (t >= n) {
-                    u = RPT;
-                    return;
-                }
-                i = LOWER ? t : n - 1 - t;
-                k = rp[i];
-                ke = rp[i + 1];
-                acc = (double)b[i * ldb] + 0.0;
-                diag = 1.0;
-                return;
+        // RPT independent row slots per lane (rows base + 32 u + lane), each advanced
+        // whenever its dependencies are ready: a later row of the claim never waits for an
+        // earlier one of the same lane (claims straddling grid lines would otherwise hold
+        // low-level rows behind high-level ones)
+        int64_t i[RPT], k[RPT], ke[RPT];
+        double acc[RPT], diag[RPT];
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+            const int64_t t = base + 32 * u + lane;
+            k[u] = ke[u] = 0;
+            i[u] = -1;
+            acc[u] = 0.0;
+            diag[u] = 1.0;
+            if (t < n) {
+                i[u] = LOWER ? t : n - 1 - t;
+                k[u] = rp[i[u]];
+                ke[u] = rp[i[u] + 1];
+                acc[u] = (double)b[i[u] * ldb] + 0.0;
             }
-        };
-        next_row();
+        }
         unsigned ns = 32;
-        while (__any_sync(0xffffffffu, u < RPT)) {
-            bool moved = false;
-            if (u < RPT) {
-                for (; k < ke; ++k) {
-                    const int64_t j = ci[k];
-                    if (LOWER ? j < i : j > i) {
+        for (;;) {
+            bool moved = false, busy = false;
+#pragma unroll
+            for (int u = 0; u < RPT; ++u) {
+                if (i[u] < 0) continue;
+                for (; k[u] < ke[u]; ++k[u]) {
+                    const int64_t j = ci[k[u]];
+                    if (LOWER ? j < i[u] : j > i[u]) {
                         V xj;
                         if constexpr (VF) {
                             if (!ld_acquire_val(x + j * ldx, xj)) break;
@@ -211,24 +214,27 @@ __global__ void __launch_bounds__(256) sptrsv_poll_kernel(int64_t n, const I *__
                             if (ld_acquire_i32(w.ready + j) == 0) break;
                             xj = __ldcg(x + j * ldx);
                         }
-                        acc = __dsub_rn(acc, mulp(val[k], xj));
-                    } else if (j == i) {
-                        diag = (double)val[k];
+                        acc[u] = __dsub_rn(acc[u], mulp(val[k[u]], xj));
+                    } else if (j == i[u]) {
+                        diag[u] = (double)val[k[u]];
                     }
                     moved = true;
                 }
-                if (k == ke) {
-                    const V xi = (LOWER && unit) ? (V)acc : (V)__ddiv_rn(acc, diag);
+                if (k[u] == ke[u]) {
+                    const V xi = (LOWER && unit) ? (V)acc[u] : (V)__ddiv_rn(acc[u], diag[u]);
                     if constexpr (VF) {
-                        st_release_val(x + i * ldx, xi);
+                        st_release_val(x + i[u] * ldx, xi);
                     } else {
-                        x[i * ldx] = xi;
-                        st_release_i32(w.ready + i, 1);
+                        x[i[u] * ldx] = xi;
+                        st_release_i32(w.ready + i[u], 1);
                     }
-                    next_row();
+                    i[u] = -1;
                     moved = true;
+                } else {
+                    busy = true;
                 }
             }
+            if (!__any_sync(0xffffffffu, busy)) break;
             if (__any_sync(0xffffffffu, moved)) {
                 ns = 32;
             } else {
@@ -280,8 +286,11 @@ cudaError_t launch_trsv(const sb_csr &T, bool lower, bool unit, const V *b, int6
     // Default: the converged-polling kernel, one row per lane (tools/precond_bench.py, IC-CG
     // ms, blocking-spin -> polling: 64^3 98 -> 84, 96^3 341 -> 284, 128^3 1058 -> 867;
     // ILU-GMRES conv-diff 64^3 137 -> 118).  SPARSEB200_TRSV_MODE=0 selects the blocking
-    // spin kernel; SPARSEB200_TRSV_RPT = 2 / 4 rows per lane (experimental: 128^3 IC-CG 588 /
-    // 430 ms, but 96^3 ~10x slower and 64^3 at 4 rows ~8x slower -- not a safe default).
+    // spin kernel; SPARSEB200_TRSV_RPT = 2 / 4 rows per lane.  Measured: processing a lane's
+    // rows strictly in order is fast where claims align with grid lines (128^3 IC-CG 430 ms
+    // at 4 rows) and ~10x slower where they straddle them (96^3: low-level rows held behind
+    // high-level ones); independent slots (the kernel above) are robust but poll more per
+    // round and gain nothing (128^3 796 / 814 / 866 ms at 1 / 2 / 4 rows), so 1 row per lane.
     static const int rpt = getenv("SPARSEB200_TRSV_RPT") ? atoi(getenv("SPARSEB200_TRSV_RPT")) : 1;
     // Mode 2 (default): polling with the value as its own flag (IC-CG 128^3 866 -> 804 ms,
     // 96^3 282 -> 261, 64^3 84 -> 78; ILU-GMRES 64^3 118 -> 109); 1: polling with separate
