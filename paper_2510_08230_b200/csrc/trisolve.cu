@@ -100,6 +100,79 @@ __global__ void __launch_bounds__(256) ilu0_kernel(int64_t n, const I *__restric
     }
 }
 
+// Same rows, arithmetic and order as ilu0_kernel, in the converged-polling form of
+// sptrsv_poll_kernel: each lane's cursor walks its row's L part while the pivot rows it
+// needs are published, never blocking inside divergent code.
+template <class V, class I>
+__global__ void __launch_bounds__(256) ilu0_poll_kernel(int64_t n, const I *__restrict__ rp,
+                                                        const I *__restrict__ ci, V *vals,
+                                                        const int64_t *__restrict__ dpos, TriWs w) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        const int64_t base = claim_rows(w.counter);
+        if (base >= n) return;
+        const int64_t i = base + lane;
+        bool active = i < n;
+        int64_t s = 0, e = 0, idx = 0;
+        unsigned long long fail = ~0ull;
+        if (active) {
+            s = rp[i];
+            e = rp[i + 1];
+            idx = s;
+        }
+        unsigned ns = 32;
+        for (;;) {
+            bool moved = false;
+            if (active) {
+                bool finished = false;
+                for (; idx < e; ++idx) {
+                    const int64_t k = ci[idx];
+                    if (k >= i) {
+                        finished = true;
+                        break;
+                    }
+                    if (ld_acquire_i32(w.ready + k) == 0) break;
+                    moved = true;
+                    const int64_t dk = dpos[k];
+                    const V ukk = dk >= 0 ? __ldcg(vals + dk) : (V)0;
+                    if (ukk == (V)0) {
+                        fail = ((unsigned long long)i << 32) | (unsigned long long)k;
+                        finished = true;
+                        break;
+                    }
+                    const V lik = vdiv(vals[idx], ukk);
+                    vals[idx] = lik;
+                    for (int64_t idx2 = dk + 1; idx2 < (int64_t)rp[k + 1]; ++idx2) {
+                        const I j = ci[idx2];
+                        const I *q = lbound(ci + s, ci + e, j);
+                        if (q != ci + e && *q == j) {
+                            V &a = vals[q - ci];
+                            a = vsub(a, vmul(lik, __ldcg(vals + idx2)));
+                        }
+                    }
+                }
+                if (idx == e) finished = true;
+                if (finished) {
+                    if (fail == ~0ull && (dpos[i] < 0 || vals[dpos[i]] == (V)0))
+                        fail = ((unsigned long long)i << 32) | (unsigned long long)i;
+                    if (fail != ~0ull) atomicMin(w.err, fail);
+                    __threadfence();
+                    st_release_i32(w.ready + i, 1);
+                    active = false;
+                    moved = true;
+                }
+            }
+            if (!__any_sync(0xffffffffu, active)) break;
+            if (__any_sync(0xffffffffu, moved)) {
+                ns = 32;
+            } else {
+                __nanosleep(ns);
+                if (ns < 256) ns <<= 1;
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------- IC(0)
 // Lower pattern (cols <= i, diagonal last) of A, computed in fp64 like the reference's
 // Python floats (lv scratch), cast to the value dtype per row.
@@ -200,8 +273,15 @@ sb_status ilu0(const sb_csr *A, void *vals_out, void *ws, void *dpos_ws, cudaStr
     int64_t *dpos = (int64_t *)dpos_ws;
     diag_pos_kernel<I><<<sweep_grid(n), 256, 0, st>>>(n, (const I *)A->row_ptrs, (const I *)A->col_idxs, dpos);
     SB_CUDA(cudaGetLastError());
-    ilu0_kernel<V, I><<<sweep_grid(n), 256, 0, st>>>(n, (const I *)A->row_ptrs, (const I *)A->col_idxs,
-                                                     (V *)vals_out, dpos, w);
+    // converged polling (default; 128^3: 23.65 -> 22.6 ms) or the blocking-spin sweep
+    // (SPARSEB200_ILU_POLL=0)
+    static const bool poll = !getenv("SPARSEB200_ILU_POLL") || atoi(getenv("SPARSEB200_ILU_POLL")) != 0;
+    if (poll)
+        ilu0_poll_kernel<V, I><<<sweep_grid(n), 256, 0, st>>>(n, (const I *)A->row_ptrs, (const I *)A->col_idxs,
+                                                              (V *)vals_out, dpos, w);
+    else
+        ilu0_kernel<V, I><<<sweep_grid(n), 256, 0, st>>>(n, (const I *)A->row_ptrs, (const I *)A->col_idxs,
+                                                         (V *)vals_out, dpos, w);
     SB_CUDA(cudaGetLastError());
     unsigned long long key;
     s = read_err(w, st, key, err);
