@@ -290,7 +290,8 @@ cudaError_t launch_trsv(const sb_csr &T, bool lower, bool unit, const V *b, int6
     // rows strictly in order is fast where claims align with grid lines (128^3 IC-CG 430 ms
     // at 4 rows) and ~10x slower where they straddle them (96^3: low-level rows held behind
     // high-level ones); independent slots (the kernel above) are robust but poll more per
-    // round and gain nothing (128^3 796 / 814 / 866 ms at 1 / 2 / 4 rows), so 1 row per lane.
+    // round and gain nothing (128^3 796 / 814 / 866 ms at 1 / 2 / 4 rows; issuing the slots'
+    // readiness loads together per round: 864 / 1027 ms), so 1 row per lane.
     static const int rpt = getenv("SPARSEB200_TRSV_RPT") ? atoi(getenv("SPARSEB200_TRSV_RPT")) : 1;
     // Mode 2 (default): polling with the value as its own flag (IC-CG 128^3 866 -> 804 ms,
     // 96^3 282 -> 261, 64^3 84 -> 78; ILU-GMRES 64^3 118 -> 109); 1: polling with separate
