@@ -291,7 +291,8 @@ cudaError_t launch_trsv(const sb_csr &T, bool lower, bool unit, const V *b, int6
     // at 4 rows) and ~10x slower where they straddle them (96^3: low-level rows held behind
     // high-level ones); independent slots (the kernel above) are robust but poll more per
     // round and gain nothing (128^3 796 / 814 / 866 ms at 1 / 2 / 4 rows; issuing the slots'
-    // readiness loads together per round: 864 / 1027 ms), so 1 row per lane.
+    // readiness loads together per round: 864 / 1027 ms), so 1 row per lane.  The back-off
+    // cap (256 ns) is flat: 32-512 ns give 3.03-3.12 ms per lower sweep.
     static const int rpt = getenv("SPARSEB200_TRSV_RPT") ? atoi(getenv("SPARSEB200_TRSV_RPT")) : 1;
     // Mode 2 (default): polling with the value as its own flag (IC-CG 128^3 866 -> 804 ms,
     // 96^3 282 -> 261, 64^3 84 -> 78; ILU-GMRES 64^3 118 -> 109); 1: polling with separate
