@@ -201,7 +201,8 @@ struct CgPArgs {
     double *partials;  // 3 G doubles: [p.q | r.r, r.z] (+ G arrival stamps when profiling)
     unsigned long long *prof;  // optional: arrival stamps of barriers 10..27 (18 G) + CTA 0 releases
     int nnz_cap;
-    int pf;  // L2 prefetch of the next update block's operands (SPARSEB200_CG_PF=0: off)
+    int pf;  // update-phase L2 prefetch distance in blocks (SPARSEB200_CG_PF; 0 = off; 128^3:
+             // 1 / 2 / 3 blocks ahead 72.4 / 73.2 / 74.4 us per iteration)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -394,8 +395,8 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
             // 71.1 us per iteration; the same hint for the SpMV phase's gathered vectors
             // measured no better, and for the stream SpMV's matrix ranges beyond its TMA
             // ring slower: 36.0 -> 37.6 us at 128^3)
-            if (a.pf && tid < 5 && blk + G < nblk) {
-                const int64_t b0 = (blk + G) * R, b1 = b0 + R < n ? b0 + R : n;
+            if (a.pf && tid < 5 && blk + (int64_t)a.pf * G < nblk) {
+                const int64_t b0 = (blk + (int64_t)a.pf * G) * R, b1 = b0 + R < n ? b0 + R : n;
                 const V *vp = tid == 0 ? x : tid == 1 ? r : tid == 2 ? q : tid == 3 ? pnew : inv;
                 if (vp) l2_prefetch_range(vp + b0, vp + b1);
             }
