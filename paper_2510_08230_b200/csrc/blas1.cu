@@ -1,3 +1,4 @@
+#include <set>
 // blas1.cu -- BLAS-1 on dense device vectors/matrices and the library-level entry points.
 //
 // Reference: core.dot / norm2 / axpy / scal / copy_into (core.py:358-401) over
@@ -10,6 +11,16 @@
 #include "spmv_launch.cuh"
 
 namespace sb {
+
+void ensure_max_smem(const void *fn) {
+    static std::mutex mu;
+    static std::set<std::pair<const void *, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.insert({fn, dev}).second)
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+}
 
 DeviceInfo &device_info() {
     static DeviceInfo infos[64];

@@ -476,11 +476,7 @@ bool cg_persistent_launch_r(const sb_matrix &M, const CgPArgs &proto, cudaStream
     const size_t smem = 2 * StreamLayout<V, I>(R, cap).stage_bytes();
     if (smem > 200 * 1024) return false;
     auto kern = cg_persistent_kernel<V, I, R>;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        configured = true;
-    }
+    ensure_max_smem((const void *)kern);
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, R, smem) != cudaSuccess || per_sm < 1) {
         cudaGetLastError();

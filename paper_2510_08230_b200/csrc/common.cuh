@@ -313,6 +313,11 @@ struct DeviceInfo {
 };
 DeviceInfo &device_info();
 
+// Opt a kernel into 200 KB of dynamic shared memory on the CURRENT device.  The
+// attribute is per (function, device), so the memo is keyed on both (a process that
+// drives a second GPU configures it there too); thread-safe, cheap after the first call.
+void ensure_max_smem(const void *fn);
+
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 }  // namespace sb

@@ -220,8 +220,11 @@ std::string matrix_key(const sb_matrix &M) {
     }
     case SB_FMT_SELLP: {
         const sb_sellp &A = *(const sb_sellp *)M.mat;
+        // max_block_entries picks block vs chunk kernel and sets the staged capacity
+        // baked into the captured launch, so it is part of the key
         s += ptr_key({A.slice_lengths, A.slice_sets, A.col_idxs, A.values, A.row_perm}) + std::to_string(A.rows) +
-             "," + std::to_string(A.slice_size);
+             "," + std::to_string(A.slice_size) + "," + std::to_string(A.num_slices) + "," +
+             std::to_string(A.max_block_entries);
         break;
     }
     case SB_FMT_HYBRID: {

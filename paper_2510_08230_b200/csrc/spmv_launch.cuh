@@ -52,12 +52,8 @@ cudaError_t launch_csr_stream_ns(const sb_csr &A, const V *b, int64_t ldb, const
     const int cap = A.plan->nnz_cap;
     const StreamLayout<V, I> L(R, cap);
     const size_t smem = NS * L.stage_bytes();
-    static int configured = 0;
     auto kern = csr_stream_kernel<V, I, R, Epi, NS>;
-    if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        configured = 1;
-    }
+    ensure_max_smem((const void *)kern);
     int grid = persistent_grid(kern, R, smem);
     const int64_t nblk = ceil_div(A.rows, R);
     if (grid > nblk) grid = (int)nblk;
@@ -89,7 +85,7 @@ cudaError_t launch_csr_spmm(const sb_csr &A, const V *b, int64_t ldb, V *x, int6
         constexpr int R64 = 64;
         const size_t smem = 2 * StreamLayout<V, I>(R64, P.nnz_cap).stage_bytes();
         auto kern = csr_stream_spmm_kernel<V, I, R64, K>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        ensure_max_smem((const void *)kern);
         int grid = persistent_grid(kern, R64, smem);
         const int64_t nblk = ceil_div(A.rows, R64);
         if (grid > nblk) grid = (int)nblk;
@@ -99,11 +95,7 @@ cudaError_t launch_csr_spmm(const sb_csr &A, const V *b, int64_t ldb, V *x, int6
     }
     const size_t smem = 2 * StreamLayout<V, I>(R, cap).stage_bytes();
     auto kern = csr_stream_spmm_kernel<V, I, R, K>;
-    static int configured = 0;
-    if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        configured = 1;
-    }
+    ensure_max_smem((const void *)kern);
     int grid = persistent_grid(kern, R, smem);
     const int64_t nblk = ceil_div(A.rows, R);
     if (grid > nblk) grid = (int)nblk;
@@ -169,11 +161,7 @@ cudaError_t launch_csr_tile_t(const sb_csr &A, const V *b, int64_t ldb, V *x, in
     const int64_t ntiles = P.num_tiles / 2;
     constexpr size_t smem = TileLayout<V, I, C, RCAP, DIRECT>::SMEM;
     auto kern = csr_tile_kernel<V, I, NT, C, RCAP, DIRECT, PF>;
-    static int configured = 0;
-    if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        configured = 1;
-    }
+    ensure_max_smem((const void *)kern);
     int grid = persistent_grid(kern, NT, smem);
     if (grid > ntiles) grid = (int)ntiles;
     if (grid < 1) return cudaSuccess;
@@ -358,12 +346,8 @@ cudaError_t launch_sellp_stream(const sb_sellp &A, const V *b, int64_t ldb, cons
     const size_t stage = (off_c + cap_c * sizeof(I) + 15) & ~size_t(15);
     // whole slice blocks when the largest fits a 2048-entry stage, else column chunks
     auto kern = A.max_block_entries <= cap ? sellp_block_kernel<V, I, S, Epi> : sellp_chunk_kernel<V, I, S, Epi>;
-    static int configured = 0;
-    if (!configured) {
-        cudaFuncSetAttribute(sellp_block_kernel<V, I, S, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(sellp_chunk_kernel<V, I, S, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        configured = 1;
-    }
+    ensure_max_smem((const void *)sellp_block_kernel<V, I, S, Epi>);
+    ensure_max_smem((const void *)sellp_chunk_kernel<V, I, S, Epi>);
     int grid = persistent_grid(kern, 128, 2 * stage);
     const int64_t nblk = ceil_div(A.num_slices, 128 / S);
     if (grid > nblk) grid = (int)nblk;

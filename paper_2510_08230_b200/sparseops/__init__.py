@@ -16,7 +16,8 @@ from .formats import (CooMatrix, CsrMatrix, EllMatrix, HybridMatrix, SellpMatrix
                       csr_from_dense, ell_from_csr, from_scipy, from_torch, hybrid_ell_width,
                       hybrid_from_csr, sellp_from_csr, validate)
 from .linop import LinOp, apply_advanced, solve_lower_tri, solve_upper_tri
-from .mmio import read_matrix_market, write_matrix_market
+from .mmio import (DuplicateEntryWarning, MatrixMarketHeader, read_matrix_market,
+                   write_matrix_market)
 from .precond import (IcFactor, IluFactors, JacobiPreconditioner, ic0_factorize, ic_apply,
                       ilu0_factorize, ilu_apply, jacobi_create)
 from .solvers import (Bicgstab, Cg, Cgs, ConvergenceLog, Gmres, Iteration, ResidualNorm,

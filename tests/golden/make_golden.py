@@ -295,11 +295,201 @@ def factorizations():
         json.dump({"cases": meta, "errors": errs, "solver_runs": runs}, fh, indent=1, sort_keys=True)
 
 
+def _mmio_corpus():
+    """Matrix Market inputs: the bodies of the reference's own tests/test_mmio.py:26-191
+    plus the cases its parser distinguishes (explicit zeros in array bodies, several values
+    per line, non-integral / out-of-range indices, non-square symmetric shapes, ragged
+    lines, duplicates created by symmetry expansion) and a few larger random files."""
+    H = "%%MatrixMarket matrix "
+    cases = [
+        # (name, text, format, precision, index width)
+        ("basic", H + "coordinate real general\n2 2 2\n1 1 1.0\n2 2 3.0\n", "Csr"),
+        ("coo_target", H + "coordinate real general\n2 2 1\n2 1 -4.5\n", "Coo"),
+        ("symmetric", H + "coordinate real symmetric\n2 2 3\n1 1 2.0\n2 1 -1.0\n2 2 2.0\n", "Csr"),
+        ("symmetric_offdiag_only", H + "coordinate real symmetric\n2 2 2\n1 1 2.0\n2 1 -1.0\n", "Csr"),
+        ("skew", H + "coordinate real skew-symmetric\n2 2 1\n2 1 5.0\n", "Csr"),
+        ("banner_case", "%%matrixmarket MATRIX Coordinate Real General\n1 1 1\n1 1 2.0\n", "Csr"),
+        ("bad_banner", "%%Matrix matrix coordinate real general\n1 1 0\n", "Csr"),
+        ("comments_blank", H + "coordinate real general\n% a comment\n\n2 2 2\n% another\n1 1 1.5\n\n2 2 2.5\n", "Csr"),
+        ("pattern", H + "coordinate pattern general\n2 2 2\n1 2\n2 1\n", "Csr"),
+        ("integer_f32", H + "coordinate integer general\n1 2 2\n1 1 3\n1 2 -7\n", "Csr", "single"),
+        ("complex", H + "coordinate complex general\n1 1 1\n1 1 1.0 0.0\n", "Csr"),
+        ("count_mismatch", H + "coordinate real general\n2 2 3\n1 1 1.0\n", "Csr"),
+        ("index_oob", H + "coordinate real general\n2 2 1\n3 1 1.0\n", "Csr"),
+        ("index_zero", H + "coordinate real general\n2 2 1\n0 1 1.0\n", "Csr"),
+        ("bad_size", H + "coordinate real general\n2 2\n", "Csr"),
+        ("duplicates", H + "coordinate real general\n2 2 2\n1 1 1.0\n1 1 2.0\n", "Csr"),
+        ("array", H + "array real general\n2 2\n1.0\n2.0\n3.0\n4.0\n", "Csr"),
+        ("array_symmetric", H + "array real symmetric\n2 2\n1.0\n2.0\n3.0\n", "Csr"),
+        ("garbage_entry", H + "coordinate real general\n1 1 1\n1 1 abc\n", "Csr"),
+        # beyond test_mmio.py: what the parser decides that changes the canonical arrays
+        ("array_zeros", H + "array real general\n3 3\n1\n0\n0\n0\n2\n0\n5\n0\n3\n", "Csr"),
+        ("array_zeros_coo", H + "array real general\n2 3\n0\n1\n0\n0\n2\n0\n", "Coo"),
+        ("array_multi_per_line", H + "array real general\n2 2\n1.0 0.0\n3.0 4.0\n", "Csr"),
+        ("array_symmetric_zeros", H + "array real symmetric\n3 3\n4\n0\n-1\n4\n0\n4\n", "Csr"),
+        ("array_skew", H + "array real skew-symmetric\n3 3\n1\n2\n3\n", "Csr"),
+        ("array_integer", H + "array integer general\n1 3\n7\n-2\n0\n", "Csr"),
+        ("array_count", H + "array real general\n2 2\n1\n2\n3\n", "Csr"),
+        ("array_bad_token", H + "array real general\n1 2\n1\nx\n", "Csr"),
+        ("array_pattern", H + "array pattern general\n1 1\n1\n", "Csr"),
+        ("array_empty", H + "array real general\n0 0\n", "Csr"),
+        ("coord_explicit_zero", H + "coordinate real general\n2 3 3\n1 1 0.0\n2 3 1.5\n1 2 0\n", "Csr"),
+        ("coord_unsorted", H + "coordinate real general\n3 3 4\n3 1 1\n1 3 2\n2 2 3\n1 1 4\n", "Coo"),
+        ("coord_inline_comment", H + "coordinate real general\n2 2 1\n1 2 7.5 % note\n", "Csr"),
+        ("coord_float_index", H + "coordinate real general\n2 2 1\n1e0 2.0 7.5\n", "Csr"),
+        ("coord_nonintegral", H + "coordinate real general\n2 2 1\n1.5 1 1.0\n", "Csr"),
+        ("coord_ragged", H + "coordinate real general\n2 2 2\n1 1 1.0\n2 2\n", "Csr"),
+        ("coord_pattern_3cols", H + "coordinate pattern general\n2 2 1\n1 1 1.0\n", "Csr"),
+        ("coord_real_2cols", H + "coordinate real general\n2 2 1\n1 1\n", "Csr"),
+        ("coord_empty_body", H + "coordinate real general\n4 5 0\n", "Csr"),
+        ("coord_empty_but_declared", H + "coordinate real general\n4 5 1\n", "Csr"),
+        ("sym_nonsquare", H + "coordinate real symmetric\n2 3 1\n1 1 1.0\n", "Csr"),
+        ("array_sym_nonsquare", H + "array real symmetric\n2 3\n1\n2\n3\n", "Csr"),
+        ("sym_mirror_duplicate", H + "coordinate real symmetric\n2 2 2\n2 1 1.0\n1 2 2.0\n", "Csr"),
+        ("skew_diagonal", H + "coordinate real skew-symmetric\n2 2 2\n1 1 3.0\n2 1 1.0\n", "Coo"),
+        ("negative_size", H + "coordinate real general\n-2 2 0\n", "Csr"),
+        ("float_size", H + "coordinate real general\n2.0 2 0\n", "Csr"),
+        ("four_tokens", "%%MatrixMarket matrix coordinate real\n1 1 0\n", "Csr"),
+        ("field_double", H + "coordinate double general\n1 1 1\n1 1 1.0\n", "Csr"),
+        ("bad_symmetry", H + "coordinate real hermitian\n1 1 1\n1 1 1.0\n", "Csr"),
+        ("bad_object", "%%MatrixMarket vector coordinate real general\n1 1 1\n1 1 1.0\n", "Csr"),
+        ("empty_file", "", "Csr"),
+        ("missing_size", H + "coordinate real general\n% only a comment\n", "Csr"),
+        ("bad_target", H + "coordinate real general\n1 1 1\n1 1 1.0\n", "Ell"),
+        ("i64", H + "coordinate real general\n3 3 3\n3 3 1\n1 2 2\n2 1 3\n", "Csr", "double", "i64"),
+        ("f32_rounding", H + "coordinate real general\n1 2 2\n1 1 0.1\n1 2 3.4028235677973366e+38\n", "Coo", "single"),
+    ]
+    rng = np.random.default_rng(31)
+    # larger random files: coordinate general with duplicates and zeros, symmetric, array
+    n = 200
+    r = rng.integers(1, n + 1, 1500); c = rng.integers(1, n + 1, 1500)
+    v = rng.standard_normal(1500); v[rng.random(1500) < 0.05] = 0.0
+    body = "".join("%d %d %.17g\n" % t for t in zip(r, c, v))
+    cases.append(("random_general_dups", H + f"coordinate real general\n{n} {n} 1500\n" + body, "Csr"))
+    lo = r >= c
+    body = "".join("%d %d %.17g\n" % t for t in zip(r[lo], c[lo], v[lo]))
+    cases.append(("random_symmetric", H + f"coordinate real symmetric\n{n} {n} {int(lo.sum())}\n" + body, "Csr"))
+    st = r > c
+    body = "".join("%d %d %.17g\n" % t for t in zip(r[st], c[st], v[st]))
+    cases.append(("random_skew_coo", H + f"coordinate real skew-symmetric\n{n} {n} {int(st.sum())}\n" + body, "Coo"))
+    a = rng.standard_normal((20, 30)); a[rng.random((20, 30)) < 0.3] = 0.0
+    body = "".join("%.17g\n" % t for t in a.T.ravel())
+    cases.append(("random_array", H + "array real general\n20 30\n" + body, "Csr"))
+    s_ = rng.standard_normal((25, 25)); s_[rng.random((25, 25)) < 0.4] = 0.0
+    body = "".join("%.17g\n" % s_[i, j] for j in range(25) for i in range(j, 25))
+    cases.append(("random_array_symmetric", H + "array real symmetric\n25 25\n" + body, "Csr", "single"))
+    return cases
+
+
+def mmio_corpus():
+    """Run the reference reader on every corpus file; record canonical arrays, warnings
+    and error classes (tests/golden/mmio_corpus.json)."""
+    import tempfile
+    import warnings as _w
+    out = []
+    with tempfile.TemporaryDirectory() as tmp:
+        for case in _mmio_corpus():
+            name, text, fmt = case[:3]
+            prec = case[3] if len(case) > 3 else "double"
+            width = case[4] if len(case) > 4 else "i32"
+            path = os.path.join(tmp, name + ".mtx")
+            with open(path, "w") as fh:
+                fh.write(text)
+            rec = dict(name=name, text=text, format=fmt, precision=prec, index_width=width)
+            with _w.catch_warnings(record=True) as caught:
+                _w.simplefilter("always")
+                try:
+                    m = sp.read_matrix_market(REF, path, getattr(sp.Precision, prec), fmt,
+                                              getattr(sp.IndexWidth, width))
+                except Exception as exc:  # noqa: BLE001 -- the class name IS the golden
+                    rec["error"] = type(exc).__name__
+                else:
+                    rec["type"] = type(m).__name__
+                    rec["shape"] = [m.rows, m.cols]
+                    if isinstance(m, sp.CsrMatrix):
+                        rec["row_ptrs"] = m.row_ptrs.tolist()
+                    else:
+                        rec["row_idxs"] = m.row_idxs.tolist()
+                    rec["col_idxs"] = m.col_idxs.tolist()
+                    rec["values_hex"] = [float(x).hex() for x in m.values.astype(np.float64)]
+                    rec["dtype"] = str(m.values.dtype)
+                    rec["index_dtype"] = str(m.col_idxs.dtype)
+            rec["warnings"] = sorted({type(w.message).__name__ for w in caught
+                                      if issubclass(w.category, UserWarning)})
+            out.append(rec)
+        # writer: exact text for the reference's own cases and a round trip
+        wr = {}
+        m = sp.csr_from_dense(REF, np.array([[1.0, 0.0], [0.0, 3.0]]))
+        sp.write_matrix_market(m, os.path.join(tmp, "w1.mtx"))
+        wr["dense2"] = open(os.path.join(tmp, "w1.mtx")).read()
+        awkward = [0.1, 1.0 / 3.0, np.pi, 1e-300, 1e300, -2.2250738585072014e-308]
+        m = sp.coo_from_triplets(REF, 6, 1, [(i, 0, v) for i, v in enumerate(awkward)])
+        sp.write_matrix_market(m, os.path.join(tmp, "w2.mtx"))
+        wr["awkward"] = open(os.path.join(tmp, "w2.mtx")).read()
+        m = sp.coo_from_triplets(REF, 3, 3, [])
+        sp.write_matrix_market(m, os.path.join(tmp, "w3.mtx"))
+        wr["empty"] = open(os.path.join(tmp, "w3.mtx")).read()
+        m = sp.csr_from_coo(sp.coo_from_triplets(REF, 2, 2, [(0, 1, 0.5), (1, 0, 0.25)],
+                                                  sp.Precision.single))
+        sp.write_matrix_market(m, os.path.join(tmp, "w4.mtx"))
+        wr["single"] = open(os.path.join(tmp, "w4.mtx")).read()
+    with open(os.path.join(HERE, "mmio_corpus.json"), "w") as fh:
+        json.dump({"source": "reference sparseops.mmio (pkg/src/sparseops/mmio.py), "
+                             "generated by tests/golden/make_golden.py mmio_corpus",
+                   "cases": out, "writer": wr}, fh, indent=0)
+
+
+def large_pins(which):
+    """Config #4 pin: run the REFERENCE GMRES(30) + Jacobi on the
+    256^3 convection-diffusion operator (c = 0.5), b = 1, x0 = 0, rtol 1e-8, on the
+    reference's own single-thread device, and record iterations / stop reason / history.
+    Slow (~40 min); run with ``python tests/golden/make_golden.py large <name>``."""
+    import time
+    path = os.path.join(HERE, "reference_large.json")
+    data = json.load(open(path)) if os.path.exists(path) else {}
+    specs = {
+        "gmres30_jacobi_convdiff3d_256": (256, 0.5, "Gmres", 5000, 30),
+        "gmres30_jacobi_convdiff3d_128": (128, 0.5, "Gmres", 5000, 30),
+        "cg_jacobi_poisson3d_256": (256, 0.0, "Cg", 100000, None),
+    }
+    for name in which:
+        p, c, cls, max_iters, dim = specs[name]
+        n, ri, ci, v = fixtures.stencil3d_triplets(p, c)
+        t0 = time.time()
+        a = ref_csr(n, n, ri, ci, v)
+        del ri, ci, v
+        m = sp.jacobi_create(a)
+        t1 = time.time()
+        b = sp.dense_create(REF, n, 1, sp.Precision.double, 1.0)
+        x = sp.dense_create(REF, n, 1, sp.Precision.double, 0.0)
+        kw = {"krylov_dim": dim} if dim else {}
+        crit = [sp.Iteration(max_iters), sp.ResidualNorm(1e-8)]
+        log = getattr(sp, cls)(a, criteria=crit, preconditioner=m, **kw).solve(b, x)
+        t2 = time.time()
+        data[name] = dict(p=p, c=c, solver=cls.lower(), krylov_dim=dim, max_iters=max_iters,
+                          reduction_factor=1e-8, device="reference (1 thread)",
+                          iterations=log.iterations, converged=log.converged,
+                          stop_reason=log.stop_reason,
+                          final_estimate=float(log.residual_history[-1]),
+                          history_head=list(map(float, log.residual_history[:5])),
+                          setup_s=round(t1 - t0, 1), solve_s=round(t2 - t1, 1))
+        with open(path, "w") as fh:
+            json.dump(data, fh, indent=1, sort_keys=True)
+        print(name, data[name]["iterations"], data[name]["solve_s"], flush=True)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "large":
+        large_pins(sys.argv[2:])
+        sys.exit(0)
+    if len(sys.argv) > 1:
+        globals()[sys.argv[1]]()
+        sys.exit(0)
     spmv_suite()
     canonicalization()
     stencils_and_jacobi()
     blas1()
     solver_goldens()
     factorizations()
+    mmio_corpus()
     print("golden fixtures written to", HERE)

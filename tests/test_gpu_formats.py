@@ -148,7 +148,7 @@ def test_matrix_market_roundtrip(dev, tmp_path):
     rp, ci, v = fixtures.canonical_csr(30, *fixtures.random_sparse_triplets(rng, 30, 30, 0.2))
     a = csr(dev, rp, ci, v)
     path = tmp_path / "a.mtx"
-    sp.write_matrix_market(path, a)
+    sp.write_matrix_market(a, path)
     b = sp.read_matrix_market(dev, path)
     np.testing.assert_array_equal(b.row_ptrs.cpu().numpy(), rp)
     np.testing.assert_array_equal(b.values.cpu().numpy(), v)
