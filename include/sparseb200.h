@@ -427,7 +427,16 @@ typedef struct {
                                              const sb_dense *b, sb_dense *x,                     \
                                              const sb_criteria *crit, int64_t krylov_dim,        \
                                              void *workspace, sb_log *log, sb_stream_t stream,   \
-                                             sb_error *err);
+                                             sb_error *err);                                     \
+    /* CGS / BiCGSTAB with ILU / IC: both applications per iteration (solvers.py:261, :273) */ \
+    sb_status sb_cgs_solve_tri_##VN##_##IN(const sb_matrix *a, const sb_tri_precond *m,          \
+                                           const sb_dense *b, sb_dense *x,                       \
+                                           const sb_criteria *crit, void *workspace,             \
+                                           sb_log *log, sb_stream_t stream, sb_error *err);      \
+    sb_status sb_bicgstab_solve_tri_##VN##_##IN(const sb_matrix *a, const sb_tri_precond *m,     \
+                                                const sb_dense *b, sb_dense *x,                  \
+                                                const sb_criteria *crit, void *workspace,        \
+                                                sb_log *log, sb_stream_t stream, sb_error *err);
 
 SB_TRI_DECLS(float, i32)
 SB_TRI_DECLS(float, i64)

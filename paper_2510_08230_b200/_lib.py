@@ -163,6 +163,10 @@ _VI_PROTOS = {
                                         P(SbCriteria), c_vp, P(SbLog), c_vp, P(SbError)]),
     "sb_gmres_solve_tri_{v}_{i}": (c_i32, [P(SbMatrix), P(SbTriPrecond), P(SbDense), P(SbDense),
                                            P(SbCriteria), c_i64, c_vp, P(SbLog), c_vp, P(SbError)]),
+    "sb_cgs_solve_tri_{v}_{i}": (c_i32, [P(SbMatrix), P(SbTriPrecond), P(SbDense), P(SbDense),
+                                         P(SbCriteria), c_vp, P(SbLog), c_vp, P(SbError)]),
+    "sb_bicgstab_solve_tri_{v}_{i}": (c_i32, [P(SbMatrix), P(SbTriPrecond), P(SbDense), P(SbDense),
+                                              P(SbCriteria), c_vp, P(SbLog), c_vp, P(SbError)]),
 }
 _I_PROTOS = {
     "sb_csr_row_stats_{i}": (c_i32, [c_i64, c_vp, c_vp, P(SbRowStats), c_vp, P(SbError)]),

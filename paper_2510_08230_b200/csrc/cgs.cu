@@ -2,6 +2,7 @@
 #include <cmath>
 
 #include "solver_common.cuh"
+#include "trisolve.cuh"
 
 namespace sb {
 
@@ -36,10 +37,11 @@ struct CgsDirection : SkipNone {
                 P.v[w] = axpy_e(1.0, U.v[w], axpy_e(beta, Q.v[w], scal_e(b2, P.v[w])));
             }
         }
-#pragma unroll
-        for (int w = 0; w < W; ++w) PH.v[w] = inv ? vmul(P.v[w], D.v[w]) : P.v[w];
         stp<W>(u, i, U);
         stp<W>(p, i, P);
+        if (!ph) return;
+#pragma unroll
+        for (int w = 0; w < W; ++w) PH.v[w] = inv ? vmul(P.v[w], D.v[w]) : P.v[w];
         stp<W>(ph, i, PH);
     }
 };
@@ -55,17 +57,19 @@ struct CgsQ : SkipNone {
     template <int W>
     __device__ __forceinline__ void elem(int64_t i, double (&)[1]) const {
         const auto U = ldp<W>(u, i), Vv = ldp<W>(v, i), D = ldp_or_one<W>(inv, i);
-        auto X = ldp<W>(x, i);
         Pk<V, W> Q, UH;
 #pragma unroll
         for (int w = 0; w < W; ++w) {
             Q.v[w] = axpy_e(-alpha, Vv.v[w], U.v[w]);
             const V uq = axpy_e(1.0, Q.v[w], U.v[w]);
             UH.v[w] = inv ? vmul(uq, D.v[w]) : uq;
-            X.v[w] = axpy_e(alpha, UH.v[w], X.v[w]);
         }
         stp<W>(q, i, Q);
         stp<W>(uh, i, UH);
+        if (!x) return;  // tri path: uh holds u + q, M is applied by the sweeps
+        auto X = ldp<W>(x, i);
+#pragma unroll
+        for (int w = 0; w < W; ++w) X.v[w] = axpy_e(alpha, UH.v[w], X.v[w]);
         stp<W>(x, i, X);
     }
 };
@@ -138,6 +142,27 @@ struct CgsResidualPass : SkipNone {
     }
 };
 
+// x += alpha uhat (tri path: uhat came from the sweeps)
+template <class V>
+struct XAxpyAlpha : SkipNone {
+    using value_type = V;
+    const V *uh;
+    V *x;
+    double alpha;
+    __device__ __forceinline__ void prepare(const Ctl *c) { alpha = c->alpha; }
+    template <int W>
+    __device__ __forceinline__ void elem(int64_t i, double (&)[1]) const {
+        const auto UH = ldp<W>(uh, i);
+        auto X = ldp<W>(x, i);
+#pragma unroll
+        for (int w = 0; w < W; ++w) X.v[w] = axpy_e(alpha, UH.v[w], X.v[w]);
+        stp<W>(x, i, X);
+    }
+};
+
+template <class V, class I>
+sb_status tri_precond_check(const sb_tri_precond &m, sb_error *err, cudaStream_t st);
+
 template <class V, class I>
 sb_status cgs_solve(const SolveArgs &a) {
     sb_error *err = a.err;
@@ -155,10 +180,26 @@ sb_status cgs_solve(const SolveArgs &a) {
     double *part = w.partials;
     const sb_matrix M = *a.A;
     const bool fused = matrix_row_owning(M);
+    const sb_tri_precond *tri = a.tri;
+    if (tri) {
+        s = tri_precond_check<V, I>(*tri, err, a.st);
+        if (s != SB_OK) return s;
+    }
+    const TriWs tw = tri ? carve_tri_ws(tri->workspace, n) : TriWs{};
+    // z = U^{-1} L^{-1} in through the scratch vector (skipped once the loop is done)
+    auto precond = [=](const V *in, V *scratch, V *out, cudaStream_t st) -> cudaError_t {
+        cudaError_t e = launch_trsv<V, I>(*tri->l, true, tri->l_unit != 0, in, 1, scratch, 1, tw, ctl,
+                                          TRI_SKIP_DONE, st);
+        if (e != cudaSuccess) return e;
+        return launch_trsv<V, I>(*tri->u, false, false, scratch, 1, out, 1, tw, ctl, TRI_SKIP_DONE, st);
+    };
     Ctl h = initial_ctl(*a.crit, w, cap);
     LoopSpec spec;
     spec.key = "cgs" + std::to_string(sizeof(V)) + std::to_string(sizeof(I)) + "|" + matrix_key(M) +
                ptr_key({a.inv, b, x, a.ws, w.vecs, w.hist, w.small});
+    if (tri)
+        spec.key += "|tri" + std::to_string(tri->l_unit) +
+                    ptr_key({tri->l->row_ptrs, tri->l->values, tri->u->row_ptrs, tri->u->values, tri->workspace});
     spec.poll_chunk = 8;
     spec.setup = [=](cudaStream_t st) -> cudaError_t {
         cudaError_t e = matrix_apply<V, I>(M, x, 1, t, 1, EpiStore<V>{t, 1}, st);
@@ -169,11 +210,20 @@ sb_status cgs_solve(const SolveArgs &a) {
         return cudaSuccess;
     };
     spec.body = [=](cudaStream_t st) -> cudaError_t {
-        cudaError_t e = launch_ew<0>(n, ctl, part, CgsDirection<V>{{}, r, q, inv, u, p, ph, 0, false}, st);
+        // solvers.py:261 phat = M p (tri: sweeps p -> t -> phat; t is free until A uhat)
+        cudaError_t e = launch_ew<0>(n, ctl, part, CgsDirection<V>{{}, r, q, inv, u, p, tri ? nullptr : ph, 0, false}, st);
         if (e != cudaSuccess) return e;
+        if (tri && (e = precond(p, t, ph, st)) != cudaSuccess) return e;
         e = matrix_apply<V, I>(M, ph, 1, v, 1, EpiSolver<V, 1, BiSigmaFin>{v, rs, nullptr, ctl, part, {}}, st);
         if (e != cudaSuccess) return e;
-        e = launch_ew<0>(n, ctl, part, CgsQ<V>{{}, u, v, inv, q, uh, x, 0}, st);
+        if (tri) {  // :269-274 q = u - alpha v; uq = u + q (in t); uhat = M uq; x += alpha uhat
+            e = launch_ew<0>(n, ctl, part, CgsQ<V>{{}, u, v, nullptr, q, t, nullptr, 0}, st);
+            if (e != cudaSuccess) return e;
+            if ((e = precond(t, ph, uh, st)) != cudaSuccess) return e;
+            e = launch_ew<0>(n, ctl, part, XAxpyAlpha<V>{{}, uh, x, 0}, st);
+        } else {
+            e = launch_ew<0>(n, ctl, part, CgsQ<V>{{}, u, v, inv, q, uh, x, 0}, st);
+        }
         if (e != cudaSuccess) return e;
         if (fused) return matrix_apply<V, I>(M, uh, 1, t, 1, EpiCgsResidual<V>{t, r, rs, ctl, part}, st);
         e = matrix_apply<V, I>(M, uh, 1, t, 1, EpiSolverStore<V, NeverSkip>{t, ctl, {}}, st);
@@ -199,6 +249,16 @@ extern "C" {
         SB_GUARD_BEGIN                                                                             \
         return cgs_solve<V, I>(SolveArgs{a, inv_diag, b, x, crit, 0, workspace, log,               \
                                          as_stream(stream), err});                                 \
+        SB_GUARD_END                                                                               \
+    }                                                                                              \
+    sb_status sb_cgs_solve_tri_##VN##_##IN(const sb_matrix *a, const sb_tri_precond *m,            \
+                                           const sb_dense *b, sb_dense *x, const sb_criteria *crit,\
+                                           void *workspace, sb_log *log, sb_stream_t stream,       \
+                                           sb_error *err) {                                        \
+        SB_GUARD_BEGIN                                                                             \
+        SolveArgs sa{a, nullptr, b, x, crit, 0, workspace, log, as_stream(stream), err};           \
+        sa.tri = m;                                                                                \
+        return cgs_solve<V, I>(sa);                                                                \
         SB_GUARD_END                                                                               \
     }
 

@@ -20,7 +20,7 @@ from .mmio import (DuplicateEntryWarning, MatrixMarketHeader, read_matrix_market
                    write_matrix_market)
 from .precond import (IcFactor, IluFactors, JacobiPreconditioner, ic0_factorize, ic_apply,
                       ilu0_factorize, ilu_apply, jacobi_create)
-from .solvers import (Bicgstab, Cg, Cgs, ConvergenceLog, Gmres, Iteration, ResidualNorm,
+from .solvers import (Bicgstab, Cg, Cgs, ConvergenceLog, Gmres, GmresTraceEvent, Iteration, ResidualNorm,
                       SolverParams, bicgstab_solve, cg_solve, cgs_solve, check_criteria,
                       gmres_solve, givens_rotation, validate_criteria)
 

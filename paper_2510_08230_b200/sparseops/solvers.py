@@ -8,7 +8,10 @@ kernels (libsparseb200 ``sb_<solver>_solve_<value>_<index>``); the host waits on
 for the final control block and residual history.  BiCGSTAB is new (the reference
 lacks it); its exact recurrence is documented in oracle/sbref.cpp.
 
-Preconditioners that run on the device: Jacobi, or none (identity).
+Fused device loops take a sparse operator with Jacobi, ILU(0), IC(0) or no
+preconditioner.  Any other LinOp operator or preconditioner (a solver used as a
+preconditioner, a dense matrix, a user operator) and GMRES ``trace=`` run the
+reference's loop composed from device BLAS-1 kernels and ``LinOp.apply`` (composed.py).
 """
 
 from __future__ import annotations
@@ -28,10 +31,13 @@ from .formats import _SparseBase, _stream
 from .linop import LinOp
 from .precond import IcFactor, IluFactors, JacobiPreconditioner
 from .linop import tri_workspace
+from . import composed
+from .composed import GmresTraceEvent
 
 __all__ = ["Iteration", "ResidualNorm", "ConvergenceLog", "SolverParams", "check_criteria",
            "validate_criteria", "givens_rotation", "Cg", "Cgs", "Gmres", "Bicgstab",
-           "cg_solve", "cgs_solve", "gmres_solve", "bicgstab_solve", "BREAKDOWN_RTOL"]
+           "cg_solve", "cgs_solve", "gmres_solve", "bicgstab_solve", "BREAKDOWN_RTOL",
+           "GmresTraceEvent"]
 
 BREAKDOWN_RTOL = 1e-30
 STOP_RESIDUAL = "residual"
@@ -173,11 +179,26 @@ class _SolverBase(LinOp):
             self._ws = torch.zeros(need, dtype=torch.uint8, device=self.device.torch)
         return self._ws
 
+    def _composed(self, b, x, trace=None) -> ConvergenceLog:
+        """The reference loop composed from device BLAS-1 + LinOp.apply (composed.py)."""
+        chk = lambda *args: check_criteria(*args)  # noqa: E731  (late-bound, patchable)
+        m = self.preconditioner
+        if self._kind == "gmres":
+            return composed.run_gmres(self.a, b, x, self.criteria, m, self.krylov_dim, chk,
+                                      ConvergenceLog, trace)
+        run = {"cg": composed.run_cg, "cgs": composed.run_cgs,
+               "bicgstab": composed.run_bicgstab}[self._kind]
+        return run(self.a, b, x, self.criteria, m, chk, ConvergenceLog)
+
+    def _fused_operands(self) -> bool:
+        m = self.preconditioner
+        return isinstance(self.a, _SparseBase) and (
+            m is None or isinstance(m, (JacobiPreconditioner, IluFactors, IcFactor)))
+
     def solve(self, b: DenseMatrix, x: DenseMatrix) -> ConvergenceLog:
         a = self.a
-        if not isinstance(a, _SparseBase):
-            raise UnsupportedFeatureError(
-                f"device solvers need a sparse matrix operator, got {type(a).__name__}")
+        if not self._fused_operands():
+            return self._composed(b, x)
         n = a.rows
         if b.shape != (n, 1) or x.shape != (n, 1):
             raise DimensionMismatchError(
@@ -193,10 +214,6 @@ class _SolverBase(LinOp):
                 raise DimensionMismatchError("preconditioner does not match the operator")
             inv = m.inv_diag
         elif isinstance(m, (IluFactors, IcFactor)):
-            if self._kind not in ("cg", "gmres"):
-                raise UnsupportedFeatureError(
-                    f"{type(m).__name__} preconditioning runs in the device CG and GMRES; "
-                    f"use Jacobi with {self._kind}")
             l, l_unit, u = m.tri_factors()
             if l.rows != n or u.rows != n or l.values.dtype != a.values.dtype or \
                     u.values.dtype != a.values.dtype or l.index_width != a.index_width or \
@@ -207,9 +224,8 @@ class _SolverBase(LinOp):
             tws = tri_workspace(a.device, n)
             tri = (_lib.SbTriPrecond(ctypes.pointer(ls), int(l_unit), 0, ctypes.pointer(us),
                                      tws.data_ptr()), ls, us, tws)
-        else:
-            raise UnsupportedFeatureError(
-                f"{type(m).__name__} is not available on the device; use Jacobi, ILU, IC or None")
+        else:  # unreachable: _fused_operands() routed it to the composed loop
+            raise UnsupportedFeatureError(f"{type(m).__name__} preconditioner")
         # contiguous, 16-byte aligned vectors for the fused kernels (a padded stride or an
         # offset view is copied around)
         bb = b if _packed(b) else _contiguous_copy(b)
@@ -296,10 +312,8 @@ class Gmres(_SolverBase):
         super().__init__(a, criteria, preconditioner, params)
 
     def solve(self, b, x, trace=None):
-        if trace is not None:
-            raise UnsupportedFeatureError(
-                "GMRES trace callbacks need host snapshots every inner iteration; the device "
-                "solver does not provide them")
+        if trace is not None:  # host snapshots every inner iteration: the composed loop
+            return self._composed(b, x, trace)
         return super().solve(b, x)
 
 

@@ -439,6 +439,74 @@ def mmio_corpus():
                    "cases": out, "writer": wr}, fh, indent=0)
 
 
+def parity_matrix():
+    """Reference runs for the solver x preconditioner parity matrix (pkg/tests/
+    test_config.py:237-273: {Cg, Cgs, Gmres} x {None, Jacobi, Ilu, Ic} on laplacian_2d(8),
+    b = 1, [Iteration(1000), ResidualNorm(1e-6)]), the same on a nonsymmetric 3-D
+    convection-diffusion operator, generic LinOp preconditioners / operators (a solver
+    as a preconditioner, a dense operator) and GMRES trace events
+    (pkg/tests/test_acceptance.py:149-173)."""
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    from helpers import random_spd_csr  # noqa: E402  (the reference's own generator)
+
+    out, meta = {}, {}
+
+    def run(name, a, bvec, cls, precond, crit, dim=None, arrays=True):
+        n = a.rows
+        b = vec(bvec, np.float64)
+        x = sp.dense_create(REF, n, 1, sp.Precision.double, 0.0)
+        kw = {"krylov_dim": dim} if dim else {}
+        log = getattr(sp, cls)(a, criteria=crit, preconditioner=precond, **kw).solve(b, x)
+        meta[name] = dict(solver=cls, iterations=log.iterations, converged=log.converged,
+                          stop_reason=log.stop_reason)
+        out[f"{name}_history"] = np.asarray(log.residual_history, np.float64)
+        out[f"{name}_x"] = x.values.copy()
+
+    crit = [sp.Iteration(1000), sp.ResidualNorm(1e-6)]
+    n, ri, ci, v = fixtures.poisson2d_triplets(8)
+    lap = ref_csr(n, n, ri, ci, v)
+    p3, ri, ci, v = fixtures.stencil3d_triplets(10, 0.5)
+    cd = ref_csr(p3, p3, ri, ci, v)
+    makers = {"none": lambda a: None, "jacobi": sp.jacobi_create, "ilu": sp.ilu0_factorize,
+              "ic": sp.ic0_factorize}
+    for cls in ("Cg", "Cgs", "Gmres"):
+        for pname, make in makers.items():
+            run(f"lap8_{cls.lower()}_{pname}", lap, np.ones(n), cls, make(lap), crit,
+                30 if cls == "Gmres" else None)
+    for cls in ("Cgs", "Gmres"):
+        for pname in ("jacobi", "ilu"):
+            run(f"convdiff10_{cls.lower()}_{pname}", cd, np.ones(p3), cls, makers[pname](cd),
+                [sp.Iteration(1000), sp.ResidualNorm(1e-8)], 30 if cls == "Gmres" else None)
+    # a solver as the preconditioner (LinOp composition, solvers.py:172-176)
+    n16, ri, ci, v = fixtures.poisson2d_triplets(16)
+    lap16 = ref_csr(n16, n16, ri, ci, v)
+    inner = sp.Cg(lap16, criteria=[sp.Iteration(8)], preconditioner=sp.jacobi_create(lap16))
+    run("lap16_gmres10_innercg8", lap16, np.ones(n16), "Gmres", inner,
+        [sp.Iteration(300), sp.ResidualNorm(1e-6)], 10)
+    # a dense operator (the reference registers DenseMatrix as a LinOp, linop.py:78)
+    dense = sp.dense_from_array(REF, lap.to_dense())
+    run("lap8dense_cg_none", dense, np.ones(n), "Cg", None, crit)
+    # GMRES trace events (test_acceptance.py:149-173)
+    problems = [("trace_lap8", lap, np.random.default_rng(31).standard_normal(n), 5),
+                ("trace_spd50", random_spd_csr(REF, np.random.default_rng(32), 50), np.ones(50), 7)]
+    for name, a, bvec, dim in problems:
+        events = []
+        x = sp.dense_create(REF, a.rows, 1, sp.Precision.double, 0.0)
+        log, _ = sp.gmres_solve(a, vec(bvec, np.float64), x, sp.SolverParams(400, 1e-9, krylov_dim=dim),
+                                trace=events.append)
+        meta[name] = dict(solver="Gmres", iterations=log.iterations, converged=log.converged,
+                          stop_reason=log.stop_reason, krylov_dim=dim,
+                          cycles=[e.cycle for e in events], inner=[e.inner for e in events])
+        out[f"{name}_rp"], out[f"{name}_ci"], out[f"{name}_v"] = a.row_ptrs, a.col_idxs, a.values
+        out[f"{name}_b"] = bvec
+        out[f"{name}_estimates"] = np.array([e.estimate for e in events])
+        out[f"{name}_solutions"] = np.stack([e.solution for e in events])
+    np.savez_compressed(os.path.join(HERE, "parity_matrix.npz"), **out)
+    meta["_source"] = "reference sparseops run by tests/golden/make_golden.py parity_matrix"
+    with open(os.path.join(HERE, "parity_matrix.json"), "w") as fh:
+        json.dump(meta, fh, indent=1, sort_keys=True)
+
+
 def large_pins(which):
     """Config #4 pin: run the REFERENCE GMRES(30) + Jacobi on the
     256^3 convection-diffusion operator (c = 0.5), b = 1, x0 = 0, rtol 1e-8, on the

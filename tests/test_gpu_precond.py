@@ -175,8 +175,11 @@ def test_preconditioned_solvers_match_reference(dev, name):
         run["solver"] == "cg"  # CG stops on the recurrence residual (solvers.py:209-216)
 
 
-def test_unsupported_combinations(dev):
+def test_mismatched_factors(dev):
+    """Every solver takes ILU / IC factors; factors of another operator are rejected."""
     a = gen.stencil_csr(dev, 6, dim=3)
-    with pytest.raises(sp.errors.UnsupportedFeatureError):
-        sp.Bicgstab(a, criteria=[sp.Iteration(5)], preconditioner=sp.ilu0_factorize(a)).solve(
-            vec(dev, np.ones(a.rows)), out(dev, a.rows, np.float64, fill=0.0))
+    other = gen.stencil_csr(dev, 5, dim=3)
+    for cls in (sp.Cg, sp.Cgs, sp.Bicgstab, sp.Gmres):
+        with pytest.raises(sp.errors.DimensionMismatchError):
+            cls(a, criteria=[sp.Iteration(5)], preconditioner=sp.ilu0_factorize(other)).solve(
+                vec(dev, np.ones(a.rows)), out(dev, a.rows, np.float64, fill=0.0))
