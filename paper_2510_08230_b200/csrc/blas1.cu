@@ -18,8 +18,13 @@ void ensure_max_smem(const void *fn) {
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lock(mu);
-    if (done.insert({fn, dev}).second)
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (done.insert({fn, dev}).second) {
+        int optin = 0;  // B200: 227 KB per block
+        if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
+            optin < 200 * 1024)
+            optin = 200 * 1024;
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 4096);
+    }
 }
 
 DeviceInfo &device_info() {

@@ -195,6 +195,9 @@ struct EpiCgFused {
 // (and the graph loop's); only the summation order of the dots differs.
 struct CgPArgs {
     int64_t n, nnz;
+    int64_t nblk;  // row blocks: nblk = kb * G of bq or bq + 1 rows (cg_block_row)
+    int64_t bq, rem;
+    int kb;        // blocks per CTA (every CTA owns exactly kb blocks: no 13-vs-14 tail)
     const void *rp, *ci, *val, *inv;
     void *x, *r, *z, *p0, *p1, *q;
     Ctl *ctl;
@@ -278,6 +281,14 @@ __device__ __forceinline__ void grid_allreduce(double (&v)[N], double *partials,
         stamps[18 * G + (target / G - 10)] = t_rel;  // CTA 0's release time
 }
 
+// first row of block b.  Blocks are whole 32-row units (warp-aligned vector accesses):
+// blocks 0 .. rem-1 hold bq + 1 units, the others bq (bq = units / nblk, rem = units %
+// nblk precomputed on the host, units = ceil(n / 32): no division in the kernel); the
+// last block is clipped to n by the caller's row bound.
+__host__ __device__ __forceinline__ int64_t cg_block_row(int64_t b, int64_t bq, int64_t rem) {
+    return 32 * (b * bq + (b < rem ? b : rem));
+}
+
 template <class V, class I, int R>
 __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -293,7 +304,8 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
     const size_t sb = L.stage_bytes();
     const int tid = threadIdx.x;
     const int G = gridDim.x;
-    const int64_t nblk = (n + R - 1) / R;
+    const int64_t nblk = a.nblk, bq = a.bq, rem = a.rem;
+    const int kb = a.kb;
     const int64_t bid = blockIdx.x;
     const uint64_t pol = policy_evict_first();
     unsigned long long *count = &c->barrier;
@@ -309,7 +321,7 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
         V *sv = reinterpret_cast<V *>(st);
         I *sc = reinterpret_cast<I *>(st + L.off_c());
         I *sr = reinterpret_cast<I *>(st + L.off_r());
-        const int64_t r0 = blk * R, r1 = r0 + R < n ? r0 + R : n;
+        const int64_t r0 = cg_block_row(blk, bq, rem), r1 = min(cg_block_row(blk + 1, bq, rem), n);
         const int64_t k0 = rp[r0], k1 = rp[r1];
         StreamMeta m;
         m.r0 = r0;
@@ -338,6 +350,7 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
         for (int64_t blk = bid; blk < nblk; blk += G, ++seq) {
             const int s = seq & 1;
             const int64_t nxt = blk + G < nblk ? blk + G : bid;  // wrap: next SpMV's first block
+            // (every block has <= R rows: nblk >= ceil(n / R))
             if (tid == 0) issue(nxt, s ^ 1);
             mbar_wait(&bar[s], (seq >> 1) & 1);
             const unsigned char *st = smem + s * sb;
@@ -388,19 +401,22 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
         // own SpMV blocks (same moving window over memory as phase A; measured faster than
         // a balanced contiguous split, which scatters the accesses over the whole vectors)
         double part2[2] = {0.0, 0.0};
-        for (int64_t blk = bid; blk < nblk; blk += G) {
-            const int64_t i = blk * R + tid;
+        for (int j = 0; j < kb; ++j) {
+            const int64_t blk = bid + (int64_t)j * G;
+            const int64_t i = cg_block_row(blk, bq, rem) + tid;
+            const bool own = i < min(cg_block_row(blk + 1, bq, rem), n);
             // five threads hint the next block's operands into L2 (cp.async.bulk.prefetch):
             // doubles the bytes in flight of this one-row-per-thread pass (128^3: 73.2 ->
             // 71.1 us per iteration; the same hint for the SpMV phase's gathered vectors
             // measured no better, and for the stream SpMV's matrix ranges beyond its TMA
             // ring slower: 36.0 -> 37.6 us at 128^3)
-            if (a.pf && tid < 5 && blk + (int64_t)a.pf * G < nblk) {
-                const int64_t b0 = (blk + (int64_t)a.pf * G) * R, b1 = b0 + R < n ? b0 + R : n;
+            if (a.pf && tid < 5 && j + a.pf < kb) {
+                const int64_t nb = blk + (int64_t)a.pf * G;
+                const int64_t b0 = cg_block_row(nb, bq, rem), b1 = min(cg_block_row(nb + 1, bq, rem), n);
                 const V *vp = tid == 0 ? x : tid == 1 ? r : tid == 2 ? q : tid == 3 ? pnew : inv;
                 if (vp) l2_prefetch_range(vp + b0, vp + b1);
             }
-            if (i < n) {
+            if (own) {
                 const V pi = pnew[i], qi = q[i];
                 x[i] = axpy_e(alpha, pi, x[i]);
                 const V ri = axpy_e(-alpha, qi, r[i]);
@@ -442,6 +458,11 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
         pnew = t;
     }
     if (tid == 0 && bid < nblk) mbar_wait(&bar[seq & 1], (seq >> 1) & 1);  // drain the prefetch
+    if (a.prof && tid == 0) {  // SM of every CTA (profiling: arrival spread by SM / die)
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        a.prof[19 * (size_t)G + bid] = smid;
+    }
     if (bid == 0 && tid == 0) {
         c->rz = rz;
         c->beta = beta;
@@ -450,9 +471,25 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
     }
 }
 
+// max stored entries of any block of the balanced partition (the stage capacity)
+template <class I>
+__global__ void cg_block_nnz_max_kernel(const I *rp, int64_t n, int64_t nblk, int64_t bq, int64_t rem, unsigned long long *out) {
+    unsigned long long m = 0;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nblk; b += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = (int64_t)rp[min(cg_block_row(b + 1, bq, rem), n)] - (int64_t)rp[min(cg_block_row(b, bq, rem), n)];
+        m = k > (int64_t)m ? (unsigned long long)k : m;
+    }
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, m, o);
+        m = t > m ? t : m;
+    }
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
 // Launch the persistent loop if the matrix is a stream-kernel CSR whose R-row block
 // stage fits, and the grid can be co-resident (cooperative launch); false = not
-// applicable (the caller runs the graph loop).
+// applicable (the caller runs the graph loop).  The rows are cut into nblk = kb * G
+// balanced blocks (<= R rows each, whole 32-row units), so every CTA owns exactly kb blocks.
 static thread_local int g_cg_last_rows = 0;  // block rows of the last persistent launch
 
 template <class V, class I, int R>
@@ -469,34 +506,51 @@ bool cg_persistent_launch_r(const sb_matrix &M, const CgPArgs &proto, cudaStream
         return false;
     }
     if (!A.plan || A.plan->kernel != SB_CSR_STREAM || A.rows == 0) return false;
-    int cap = A.plan->block_rows == 256 ? A.plan->nnz_cap
-                                        : (A.plan->block_rows == 128 ? A.plan->nnz_cap256 : 0);
-    if (cap <= 0) return false;
-    cap *= R / 256;  // a block of R rows holds at most R / 256 times a 256-row block's cap
-    const size_t smem = 2 * StreamLayout<V, I>(R, cap).stage_bytes();
-    if (smem > 200 * 1024) return false;
     auto kern = cg_persistent_kernel<V, I, R>;
     ensure_max_smem((const void *)kern);
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, R, smem) != cudaSuccess || per_sm < 1) {
+    const int sms = device_info().sms;
+    const int per_sm = 1024 / R;
+    int64_t grid = (int64_t)per_sm * sms;
+    const int64_t nb_min = ceil_div(A.rows, R);
+    if (grid > nb_min) grid = nb_min;
+    if (grid > kMaxGrid) grid = kMaxGrid;
+    const int64_t kb = ceil_div(nb_min, grid);
+    const int64_t nblk = kb * grid;
+    if (nblk > ceil_div(A.rows, 32)) return false;  // tiny systems: fewer units than blocks
+    // stage capacity of the balanced blocks (one pass over nblk row pointers)
+    unsigned long long *dmax = &proto.ctl->tphase[9];
+    if ((err = cudaMemsetAsync(dmax, 0, sizeof(*dmax), st)) != cudaSuccess) return false;
+    cg_block_nnz_max_kernel<I><<<(unsigned)std::min<int64_t>(ceil_div(nblk, 256), 1024), 256, 0, st>>>(
+        (const I *)A.row_ptrs, A.rows, nblk, ceil_div(A.rows, 32) / nblk, ceil_div(A.rows, 32) % nblk, dmax);
+    unsigned long long hmax = 0;
+    if ((err = cudaMemcpyAsync(&hmax, dmax, sizeof(hmax), cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (err = cudaStreamSynchronize(st)) != cudaSuccess)
+        return false;
+    if (hmax > (1u << 20)) return false;
+    const int cap = (int)((hmax + 63) & ~63ull);
+    const size_t smem = 2 * StreamLayout<V, I>(R, cap > 0 ? cap : 64).stage_bytes();
+    if (smem > 220 * 1024) return false;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, R, smem) != cudaSuccess || occ < per_sm) {
         cudaGetLastError();
         return false;
     }
-    const int64_t nblk = ceil_div(A.rows, R);
-    int64_t grid = (int64_t)per_sm * device_info().sms;
-    if (grid > nblk) grid = nblk;
-    if (grid > kMaxGrid) grid = kMaxGrid;
     CgPArgs args = proto;
     args.n = A.rows;
     args.nnz = A.nnz;
     args.rp = A.row_ptrs;
     args.ci = A.col_idxs;
     args.val = A.values;
-    args.nnz_cap = cap;
+    args.nnz_cap = cap > 0 ? cap : 64;
+    args.nblk = nblk;
+    args.bq = ceil_div(A.rows, 32) / nblk;
+    args.rem = ceil_div(A.rows, 32) % nblk;
+    args.kb = (int)kb;
     void *params[] = {&args};
     err = cudaLaunchCooperativeKernel((const void *)kern, dim3((unsigned)grid), dim3(R), params, smem, st);
     if (err != cudaSuccess) {
         cudaGetLastError();
+        err = cudaSuccess;
         return false;  // not co-resident here: graph loop instead
     }
     g_cg_last_rows = R;
@@ -505,16 +559,22 @@ bool cg_persistent_launch_r(const sb_matrix &M, const CgPArgs &proto, cudaStream
 
 template <class V, class I>
 bool cg_persistent_launch(const sb_matrix &M, const CgPArgs &proto, cudaStream_t st, cudaError_t &err) {
+    err = cudaSuccess;
     // Small systems (<= 2^20 rows): 512-row blocks (2 CTAs of 512 threads per SM: half the
     // barrier arrivals) where their stage fits; else 256 (cg_modes.py, us per iteration,
     // 256 -> 512 rows: 64^3 15.6 -> 14.5-14.8, 96^3 32.8 -> 32.0-32.3; 128^3 72.2 ->
     // 72.2-72.4 and bench.py 13.80k -> 13.62-13.74k iterations/s).  SPARSEB200_CG_R = 256 /
-    // 512 forces one.
+    // 512 forces one.  Measured and dropped (profiles/README.md, round 2): the residual
+    // kept in shared memory (two CTAs per SM: 94 vs 73 us per iteration at 128^3 -- the
+    // update pass needs the occupancy for its loads in flight), L2 eviction-priority hints
+    // per vector, L2 prefetch of phase-B operands before barrier 1 / of further matrix
+    // blocks before barrier 2, and walking the update blocks backwards: all flat or slower.
     static const int r_env = getenv("SPARSEB200_CG_R") ? atoi(getenv("SPARSEB200_CG_R")) : 0;
     const int64_t rows = M.format == SB_FMT_CSR ? ((const sb_csr *)M.mat)->rows
                                                 : (M.format == SB_FMT_COO ? ((const sb_coo *)M.mat)->rows : 0);
     const int r = r_env ? r_env : (rows <= (int64_t(1) << 20) ? 512 : 256);
     if (r == 512 && cg_persistent_launch_r<V, I, 512>(M, proto, st, err)) return true;
+    if (err != cudaSuccess) return false;
     return cg_persistent_launch_r<V, I, 256>(M, proto, st, err);
 }
 
@@ -732,8 +792,14 @@ sb_status cg_solve(const SolveArgs &a) {
                         h.tphase[2] * 1e-3 / h.iter, h.tphase[3] * 1e-3 / h.iter);
             if (prof && h.iter > 14) {  // per barrier: arrival spread, CTA-0 wait, wake-up
                 const int G = (int)h.tphase[4];
-                std::vector<unsigned long long> st(19 * (size_t)G);
+                std::vector<unsigned long long> st(20 * (size_t)G);
                 SB_CUDA(cudaMemcpy(st.data(), pa.prof, st.size() * 8, cudaMemcpyDeviceToHost));
+                if (const char *dump = getenv("SPARSEB200_CG_PROFILE_DUMP")) {  // raw stamps
+                    if (FILE *f = fopen(dump, "wb")) {
+                        fwrite(st.data(), 8, st.size(), f);
+                        fclose(f);
+                    }
+                }
                 for (int e = 0; e < 18 && 10 + e <= 2 * h.iter; ++e) {
                     unsigned long long lo = ~0ull, hi = 0;
                     int slow = 0;
@@ -749,6 +815,7 @@ sb_status cg_solve(const SolveArgs &a) {
             }
             return finish_log(h, a, w);
         }
+        SB_CUDA(le);
         // not applicable: fall through to the graph loop (setup is re-run by run_loop)
     }
     LoopSpec spec;
