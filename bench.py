@@ -15,11 +15,14 @@ against the measured HBM copy bandwidth in MEASURED_PEAKS.json.  `cpu_baseline` 
 the oracle port (oracle/sbref.cpp) of the reference's CG on this host's cores for a
 bounded sample of iterations.
 
-Multi-GPU (torchrun, N > 1): the SAME global system is row-partitioned across the N
-GPUs (paper_2510_08230_b200.dist: NCCL halo exchange overlapped with the interior
-SpMV, ncclAllReduce of the fused dots) -> strong scaling; `value` stays global CG
-iterations per second.  `--workload cg512` selects BASELINE config #5 (Poisson 512^3,
-134M rows), the north_star strong-scaling problem.
+Multi-GPU (N > 1; under torchrun, or `--gpus N` alone, which re-launches itself through
+torch.distributed.run with N ranks): the SAME global system is row-partitioned across
+the N GPUs (paper_2510_08230_b200.dist: NCCL halo exchange overlapped with the interior
+SpMV, ncclAllReduce of the local dots, the graph-loop DistCg of csrc/dist_krylov.cu) ->
+strong scaling; `value` stays global CG iterations per second.  The default workload is
+cg128 at EVERY N, so the driver's 1/2/4/8 series is one problem (strong scaling of
+config #2; latency-bound beyond 2-4 GPUs at 2.1M rows).  `--workload cg512` selects
+BASELINE config #5 (Poisson 512^3, 134M rows), the north_star strong-scaling problem.
 """
 
 from __future__ import annotations
@@ -430,7 +433,7 @@ def run_partitioned(args, world, rank, local):
             "roofline": roofline, "cpu_baseline": None,
             "e2e": {"value": e_iters / (e_ms / 1e3), "unit": "CG iters/s",
                     "h2d_bytes_per_step": 2 * 8 * nl, "d2h_bytes_per_step": 8 * nl},
-            "gpu_launches": args.steps * (6 + 8 * log.iterations),
+            "gpu_launches": args.steps * (8 + 10 * log.iterations),
             "clocks": clocks.summary(),
         }
         print(json.dumps(line))
@@ -452,8 +455,25 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     else:
         run_ours(args)
+
+
+def spawn_ranks(args):
+    """`bench.py --gpus N` without a launcher: re-run this script under
+    torch.distributed.run with N ranks on this node (rendezvous on 127.0.0.1); rank 0's
+    JSON line passes through on stdout."""
+    import socket
+    import subprocess
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

@@ -367,14 +367,27 @@ sb_status sb_nccl_comm_destroy(void *comm, sb_error *err);
 size_t sb_dist_workspace_bytes(int32_t value_bytes, int64_t n_local, int64_t n_ghost,
                                int64_t history_cap);
 
-/* Row-partitioned Jacobi-CG (solvers.py:188-224 semantics): halo exchange of the search
- * direction per SpMV (overlapped with the interior rows), fused local dots combined with
+/* workspace of one partition for solver kind SB_SOLVER_CG / _BICGSTAB / _GMRES
+ * (sb_dist_workspace_bytes == the CG size) */
+size_t sb_dist_solver_workspace_bytes(int32_t solver, int32_t value_bytes, int64_t n_local,
+                                      int64_t n_ghost, int64_t krylov_dim, int64_t history_cap);
+
+/* Row-partitioned Jacobi-preconditioned solvers with the single-GPU solvers' semantics
+ * (CG solvers.py:188-224, GMRES(m) :322-399, BiCGSTAB oracle/sbref.cpp): halo exchange of
+ * every SpMV input (overlapped with the interior rows), fused local dots combined with
  * ncclAllReduce (comm != NULL, nparts == 1) or summed across `nparts` partitions living
- * on this one GPU (comm == NULL: the loopback transport that tests the decomposition). */
+ * on this one GPU (comm == NULL: the loopback transport that tests the decomposition).
+ * inv_diag == NULL in a partition = no preconditioner. */
 #define SB_DIST_DECLS(VN, IN)                                                                    \
     sb_status sb_dist_cg_solve_##VN##_##IN(sb_dist_part *parts, int32_t nparts, void *comm,       \
                                            const sb_criteria *crit, sb_log *log,                  \
-                                           sb_stream_t stream, sb_error *err);
+                                           sb_stream_t stream, sb_error *err);                    \
+    sb_status sb_dist_bicgstab_solve_##VN##_##IN(sb_dist_part *parts, int32_t nparts, void *comm, \
+                                                 const sb_criteria *crit, sb_log *log,            \
+                                                 sb_stream_t stream, sb_error *err);              \
+    sb_status sb_dist_gmres_solve_##VN##_##IN(sb_dist_part *parts, int32_t nparts, void *comm,    \
+                                              const sb_criteria *crit, int64_t krylov_dim,        \
+                                              sb_log *log, sb_stream_t stream, sb_error *err);
 SB_DIST_DECLS(float, i32)
 SB_DIST_DECLS(float, i64)
 SB_DIST_DECLS(double, i32)

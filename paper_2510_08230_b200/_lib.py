@@ -152,6 +152,10 @@ _VI_PROTOS = {
                                        c_i64, c_vp, P(SbLog), c_vp, P(SbError)]),
     "sb_dist_cg_solve_{v}_{i}": (c_i32, [P(SbDistPart), c_i32, c_vp, P(SbCriteria), P(SbLog),
                                          c_vp, P(SbError)]),
+    "sb_dist_bicgstab_solve_{v}_{i}": (c_i32, [P(SbDistPart), c_i32, c_vp, P(SbCriteria), P(SbLog),
+                                               c_vp, P(SbError)]),
+    "sb_dist_gmres_solve_{v}_{i}": (c_i32, [P(SbDistPart), c_i32, c_vp, P(SbCriteria), c_i64,
+                                            P(SbLog), c_vp, P(SbError)]),
     "sb_csr_trisolve_{v}_{i}": (c_i32, [P(SbCsr), c_i32, c_i32, P(SbDense), P(SbDense), c_vp, c_vp,
                                         P(SbError)]),
     "sb_csr_tri_check_{v}_{i}": (c_i32, [P(SbCsr), c_i32, c_i32, c_vp, c_vp, P(SbError)]),
@@ -199,6 +203,7 @@ _PLAIN_PROTOS = {
     "sb_nccl_comm_init": (c_i32, [c_i32, ctypes.c_char_p, c_i32, P(c_vp), P(SbError)]),
     "sb_nccl_comm_destroy": (c_i32, [c_vp, P(SbError)]),
     "sb_dist_workspace_bytes": (c_sz, [c_i32, c_i64, c_i64, c_i64]),
+    "sb_dist_solver_workspace_bytes": (c_sz, [c_i32, c_i32, c_i64, c_i64, c_i64, c_i64]),
 }
 
 

@@ -55,7 +55,7 @@ struct Ctl {
     double *hcol, *g, *cs, *sn, *y, *R;  // R: dim x dim, row-major
     double hnorm, beta_restart;
     int64_t cycle;
-    double dot[8];  // row-partitioned solves: local dot totals, reduced across ranks in place
+    double dot[24];  // row-partitioned solves: local dot totals, reduced across ranks in place
     unsigned long long tphase[10];  // persistent CG: CTA 0's ns per phase, summed over iterations
     unsigned long long barrier;    // persistent CG: grid-barrier arrivals (0 at every solve start)
 };
@@ -330,6 +330,7 @@ struct LoopSpec {
     int poll_chunk;                                    // iterations per host poll (fallback)
     void *hot_base = nullptr;                          // L2-persisting window (work vectors)
     size_t hot_bytes = 0;
+    bool local_fallback = false;  // graph build failure polls this loop only (NCCL bodies)
 };
 
 // Writes the initial control block (with the loop's conditional handle), enqueues

@@ -124,7 +124,14 @@ sb_status run_loop(const LoopSpec &spec, Ctl *dctl, Ctl &hctl, cudaStream_t st, 
                 g_pdl = 0;
                 e = build_while_graph(spec, fresh);
             }
-            if (e != cudaSuccess) {
+            if (e != cudaSuccess && spec.local_fallback) {
+                // e.g. a collective that cannot be captured into a conditional body: poll
+                // this loop, keep graphs for everything else
+                fprintf(stderr, "[sparseb200] graph loop unavailable for this solve (%s); polling\n",
+                        cudaGetErrorString(e));
+                cudaGetLastError();
+                use_graph = false;
+            } else if (e != cudaSuccess) {
                 // conditional nodes unavailable: fall back to host polling for good
                 fprintf(stderr, "[sparseb200] graph loop unavailable (%s); using polled launches\n",
                         cudaGetErrorString(e));

@@ -10,7 +10,11 @@ that read ghosts form a prefix and a suffix of the local block (true for slab
 partitions of the stencils), the SpMV is split into an interior view that runs while
 the halo is in flight and the boundary views that run after it.
 
-Transports (libsparseb200 ``sb_dist_cg_solve_*``):
+Solvers (libsparseb200 ``sb_dist_{cg,bicgstab,gmres}_solve_*``, csrc/dist_krylov.cu):
+DistCg, DistBicgstab, DistGmres -- the single-GPU solvers' fused steps on the local rows,
+every reduction's local totals summed across ranks before the unchanged finaliser runs.
+
+Transports:
 * NCCL: one rank per GPU, grouped ncclSend/ncclRecv halos and ncclAllReduce of the fused
   dot partials, captured into CUDA graphs (``NcclComm`` builds the communicator; the
   unique id travels through torch.distributed);
@@ -37,7 +41,7 @@ from .sparseops.formats import CsrMatrix, _ptr, _stream
 from .sparseops.solvers import ConvergenceLog, _criteria_struct, validate_criteria
 
 __all__ = ["partition", "LocalPattern", "localize", "exchange_send_lists", "DistPartition",
-           "stencil_partition", "csr_partition", "NcclComm", "DistCg"]
+           "stencil_partition", "csr_partition", "NcclComm", "DistCg", "DistBicgstab", "DistGmres"]
 
 
 def partition(n: int, parts: int) -> list[tuple[int, int]]:
@@ -148,7 +152,12 @@ class DistPartition:
         self.views, self.view_row0 = [], []
         if split is not None and ng > 0 and nl > 0:
             pre, suf = split
-            ranges = [(pre, nl - suf), (0, pre), (nl - suf, nl)]
+            # view boundaries on multiples of 4 rows: every view's row_ptrs slice (and its
+            # output offset) stays 16-byte aligned for the TMA-staged SpMV; moving rows from
+            # the interior view into a boundary view is always correct
+            pre = min(nl, (pre + 3) // 4 * 4)
+            tail0 = max(pre, (nl - suf) // 4 * 4)
+            ranges = [(pre, tail0), (0, pre), (tail0, nl)]
             for a, b in ranges:
                 if b > a:
                     self.views.append(CsrMatrix(device, b - a, nl + ng, self.matrix.row_ptrs[a:b + 1],
@@ -201,10 +210,11 @@ class DistPartition:
                        self.matrix.values, kernel="strict")
         return jacobi_create(sq).inv_diag
 
-    def struct(self, b, x, cap: int) -> _lib.SbDistPart:
-        if self.workspace is None or self.workspace.numel() < self._ws_bytes(cap):
-            self.workspace = torch.zeros(self._ws_bytes(cap), dtype=torch.uint8,
-                                         device=self.device.torch)
+    def struct(self, b, x, cap: int, kind: int = _lib.SOLVER_CG, dim: int = 0,
+               precond: bool = True) -> _lib.SbDistPart:
+        need = self._ws_bytes(cap, kind, dim)
+        if self.workspace is None or self.workspace.numel() < need:
+            self.workspace = torch.zeros(need, dtype=torch.uint8, device=self.device.torch)
         P = _lib.SbDistPart()
         P.a = self.matrix.matrix_struct()
         P.num_views = len(self.views)
@@ -219,15 +229,15 @@ class DistPartition:
         P.recv_count, P.recv_off = h["recv_count"], h["recv_off"]
         P.send_idx = self.send_idx.data_ptr()
         P.send_buf = self.send_buf.data_ptr()
-        P.inv_diag = self.inv_diag.data_ptr() if self.inv_diag is not None else None
+        P.inv_diag = self.inv_diag.data_ptr() if (precond and self.inv_diag is not None) else None
         P.b = b.struct()
         P.x = x.struct()
         P.workspace = self.workspace.data_ptr()
         return P
 
-    def _ws_bytes(self, cap):
-        return int(_lib.fn("sb_dist_workspace_bytes")(self.matrix.precision.itemsize, self.n_local,
-                                                       self.n_ghost, cap))
+    def _ws_bytes(self, cap, kind=_lib.SOLVER_CG, dim=0):
+        return int(_lib.fn("sb_dist_solver_workspace_bytes")(kind, self.matrix.precision.itemsize,
+                                                              self.n_local, self.n_ghost, dim, cap))
 
 
 def stencil_partition(device: Device, p: int, rank: int, world: int, dim: int = 3, c: float = 0.0,
@@ -306,16 +316,27 @@ class NcclComm:
             self.handle = ctypes.c_void_p()
 
 
-class DistCg:
-    """Row-partitioned Jacobi-CG.  ``parts``: this rank's DistPartition (with ``comm``)
-    or every partition of the system on this GPU (loopback, comm=None)."""
+class _DistSolver:
+    """Row-partitioned Krylov solve.  ``parts``: this rank's DistPartition (with ``comm``)
+    or every partition of the system on this GPU (loopback, comm=None).  Jacobi
+    preconditioning from each partition's local inverse diagonal (``jacobi=False``: none)."""
 
-    def __init__(self, parts, criteria, comm: NcclComm | None = None):
+    _kind = None
+    _name = None
+
+    def __init__(self, parts, criteria, comm: NcclComm | None = None, jacobi: bool = True):
         self.parts = list(parts) if isinstance(parts, (list, tuple)) else [parts]
         self.criteria = validate_criteria(criteria)
         self.comm = comm
+        self.jacobi = jacobi
         if comm is not None and len(self.parts) != 1:
             raise E.InvalidArgumentError("NCCL mode takes exactly one partition per rank")
+
+    def _extra(self):
+        return ()
+
+    def _dim(self):
+        return 0
 
     def solve(self, bs, xs) -> ConvergenceLog:
         bs = bs if isinstance(bs, (list, tuple)) else [bs]
@@ -327,11 +348,46 @@ class DistCg:
         n = len(self.parts)
         arr = (_lib.SbDistPart * n)()
         for k, (part, b, x) in enumerate(zip(self.parts, bs, xs)):
-            arr[k] = part.struct(b, x, cap)
+            arr[k] = part.struct(b, x, cap, self._kind, self._dim(), self.jacobi)
         m = self.parts[0].matrix
         comm = self.comm.handle if self.comm is not None else ctypes.c_void_p()
-        _lib.call(f"sb_dist_cg_solve_{m.precision.suffix}_{m.index_width.suffix}", arr, n, comm,
-                  ctypes.byref(crit), ctypes.byref(log), _stream(self.parts[0].device))
+        _lib.call(f"sb_dist_{self._name}_solve_{m.precision.suffix}_{m.index_width.suffix}", arr, n, comm,
+                  ctypes.byref(crit), *self._extra(), ctypes.byref(log), _stream(self.parts[0].device))
         hl = min(int(log.history_len), cap)
         return ConvergenceLog(int(log.iterations), hist[:hl].tolist(), bool(log.converged),
                               "residual" if log.stop_reason == 0 else "max_iters")
+
+
+class DistCg(_DistSolver):
+    """Row-partitioned (Jacobi-)CG: 2 allreduces per iteration (p.q; r.r + r.z)."""
+
+    _kind = _lib.SOLVER_CG
+    _name = "cg"
+
+
+class DistBicgstab(_DistSolver):
+    """Row-partitioned (Jacobi-)BiCGSTAB: 2 halos and 4 allreduces per iteration."""
+
+    _kind = _lib.SOLVER_BICGSTAB
+    _name = "bicgstab"
+
+
+class DistGmres(_DistSolver):
+    """Row-partitioned (Jacobi-)GMRES(krylov_dim): single-pass MGS with one allreduce per
+    step (the reference's order, solvers.py:353-358)."""
+
+    _kind = _lib.SOLVER_GMRES
+    _name = "gmres"
+
+    def __init__(self, parts, criteria, comm: NcclComm | None = None, krylov_dim: int = 30,
+                 jacobi: bool = True):
+        if krylov_dim < 1:
+            raise E.InvalidArgumentError("krylov_dim must be positive")
+        self.krylov_dim = int(krylov_dim)
+        super().__init__(parts, criteria, comm, jacobi)
+
+    def _dim(self):
+        return self.krylov_dim
+
+    def _extra(self):
+        return (self.krylov_dim,)
