@@ -146,6 +146,44 @@ def cpu_baseline_sample(iters=60):
                       f"oracle/sbref.cpp (C++ restatement of the reference), {dt:.2f} s"}
 
 
+def reference_numba_sample(iters=20):
+    """The reference ITSELF (sparseops, pure Python + numba, installed unmodified into
+    baseline/_ref by `pip install --no-deps --target baseline/_ref`) running its own
+    Jacobi-CG (solvers.py:188-224) on the `omp` device with every host thread
+    (BASELINE.md §4): a fixed-iteration sample at 128^3 -> iterations/s.  None when the
+    install is absent.  Matrix construction and jacobi_create are outside the timing."""
+    path = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "sparseops")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_sparseops")
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import sparseops as ref  # the reference (top-level name; ours is paper_2510_08230_b200.sparseops)
+    except Exception:
+        return None
+    from oracle import fixtures
+
+    threads = len(os.sched_getaffinity(0))
+    n, ri, ci, v = fixtures.stencil3d_triplets(P)
+    dev = ref.create_device("omp", threads=threads)
+    t0 = time.perf_counter()
+    a = ref.csr_from_coo(ref.coo_from_arrays(dev, n, n, ri, ci, v, ref.Precision.double, ref.IndexWidth.i32))
+    m = ref.jacobi_create(a)
+    setup = time.perf_counter() - t0
+    b = ref.dense_create(dev, n, 1, ref.Precision.double, 1.0)
+    x = ref.dense_create(dev, n, 1, ref.Precision.double, 0.0)
+    ref.Cg(a, criteria=[ref.Iteration(2)], preconditioner=m).solve(b, x)  # numba JIT warm-up
+    x = ref.dense_create(dev, n, 1, ref.Precision.double, 0.0)
+    t0 = time.perf_counter()
+    log = ref.Cg(a, criteria=[ref.Iteration(iters)], preconditioner=m).solve(b, x)
+    dt = time.perf_counter() - t0
+    return {"value": log.iterations / dt, "unit": "CG iters/s", "cores": threads, "kind": "reference",
+            "sample": f"{log.iterations} fixed Jacobi-CG iterations, fp64 Poisson 128^3, the reference "
+                      f"sparseops (numba) on omp[{threads}] from baseline/_ref, {dt:.2f} s "
+                      f"(setup incl. jacobi_create {setup:.1f} s, untimed)"}
+
+
 def run_reference(args):
     world, rank, _ = _dist()
     if world > 1:
@@ -166,6 +204,7 @@ def run_reference(args):
             "config": {"workload": "Jacobi-CG fp64 3-D 7-pt Poisson 128^3, rtol 1e-8 "
                                    "(fixed-iteration CPU sample of 30 iterations per step)"},
             "cpu_baseline": {**base, "value": v},
+            "reference_numba": reference_numba_sample(),
             "e2e": {"value": v, "unit": "CG iters/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -324,6 +363,7 @@ def run_ours(args):
     assert abs(float(xh[n // 2]) - float(x.values[n // 2])) <= 1e-6 * abs(float(x.values[n // 2]))
 
     cpu = cpu_baseline_sample() if not args.no_cpu and p == 128 else None
+    cpu_ref = reference_numba_sample() if not args.no_cpu and p == 128 else None
     line = {
         "metric": METRIC, "value": value, "unit": "CG iters/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -345,6 +385,7 @@ def run_ours(args):
                  "traffic": spmv_roof["traffic"]},
         "roofline": roofline,
         "cpu_baseline": cpu,
+        "cpu_baseline_reference_numba": cpu_ref,
         "e2e": {"value": e2e_value, "unit": "CG iters/s", "h2d_bytes_per_step": 2 * 8 * n,
                 "d2h_bytes_per_step": 8 * n + 64},
         "gpu_launches": launches,
