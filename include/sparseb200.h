@@ -205,6 +205,13 @@ void sb_set_graph_mode(int enabled);
    0 = three kernels per iteration (SpMV+dot, update, direction).  Modes 0 and 1 give
    bitwise identical iterates; 3 differs only in the summation order of the dots. */
 void sb_set_cg_fused(int mode);
+/* Grid barriers per iteration of the persistent CG kernel: 2 (default) = SpMV phase and
+   update phase; 1 = single-sync kernel (the update of iteration k-1 re-evaluated at every
+   out-of-block gathered column of SpMV k, beta from an exact algebraic expansion of r.z:
+   A + 9 V n bytes per iteration; stored vector elements computed with the same rounding
+   steps, beta within a few ulps; measured slower on B200, kept opt-in).  Replaces nothing
+   in the reference (solvers.py:188-224 is one loop shape). */
+void sb_set_cg_sync(int barriers);
 /* Loop shape used by this thread's last CG solve: 0 three-kernel graph loop, 1 fused-
    direction graph loop, 3 persistent cooperative kernel (one launch per solve). */
 int sb_cg_last_loop(void);

@@ -23,7 +23,10 @@ void ensure_max_smem(const void *fn) {
         if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
             optin < 200 * 1024)
             optin = 200 * 1024;
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 4096);
+        cudaFuncAttributes fa{};  // the opt-in limit covers static + dynamic shared memory
+        const size_t stat = cudaFuncGetAttributes(&fa, fn) == cudaSuccess ? fa.sharedSizeBytes : 4096;
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)stat);
+        cudaGetLastError();
     }
 }
 

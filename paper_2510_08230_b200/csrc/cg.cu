@@ -88,6 +88,7 @@ struct CgPArgs {
     int nnz_cap;
     int pf;  // update-phase L2 prefetch distance in blocks (SPARSEB200_CG_PF; 0 = off; 128^3:
              // 1 / 2 / 3 blocks ahead 72.4 / 73.2 / 74.4 us per iteration)
+    void *q1;  // single-sync kernel: second q buffer (z doubles as the second r buffer)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -140,7 +141,7 @@ __device__ __forceinline__ void grid_allreduce(double (&v)[N], double *partials,
     double a[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) a[k] = 0.0;
-    constexpr int U = 4;  // independent loads in flight per thread (G <= U R covers 1024 CTAs)
+    constexpr int U = N > 2 ? 1 : 4;  // independent loads in flight per thread (registers: N U doubles)
     for (int i0 = threadIdx.x; i0 < G; i0 += U * R) {
         double t[N][U];
 #pragma unroll
@@ -192,6 +193,15 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
     const uint64_t pol = policy_evict_first();
     unsigned long long *count = &c->barrier;
     unsigned long long epoch = 0;  // barriers passed in this launch
+    // row-pointer bounds of this CTA's kb blocks, loaded once: issue() then starts its bulk
+    // copies without a dependent global load (thread 0 was a full L2 round trip behind
+    // the other threads of every block, which the block-end __syncthreads exposed)
+    int64_t *kbnd = reinterpret_cast<int64_t *>(smem + 2 * sb);
+    for (int q2 = tid; q2 < kb; q2 += R) {
+        const int64_t blk = bid + (int64_t)q2 * G;
+        kbnd[2 * q2] = rp[cg_block_row(blk, bq, rem)];
+        kbnd[2 * q2 + 1] = rp[min(cg_block_row(blk + 1, bq, rem), n)];
+    }
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -204,7 +214,8 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
         I *sc = reinterpret_cast<I *>(st + L.off_c());
         I *sr = reinterpret_cast<I *>(st + L.off_r());
         const int64_t r0 = cg_block_row(blk, bq, rem), r1 = min(cg_block_row(blk + 1, bq, rem), n);
-        const int64_t k0 = rp[r0], k1 = rp[r1];
+        const int64_t q2 = (blk - bid) / G;
+        const int64_t k0 = kbnd[2 * q2], k1 = kbnd[2 * q2 + 1];
         StreamMeta m;
         m.r0 = r0;
         m.r1 = r1;
@@ -353,6 +364,251 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
     }
 }
 
+// ---------------------------------------------------------------- single-sync persistent CG
+// The same CG with ONE grid barrier per iteration.  Phase j (one SpMV) no longer waits
+// for the update of iteration j-1: every gathered column re-evaluates that update on the
+// fly from the previous phase's vectors,
+//     r_j = r_{j-1} - alpha_{j-1} q_{j-1},  z_j = M r_j,  p_j = z_j + beta_{j-1} p_{j-1},
+// with the reference's rounding of each step (axpy; vmul; scal then axpy), so every
+// element of r, z, p, q and x is bitwise what the two-barrier loop stores.  The CTA
+// owning row i stores r_j, p_j, q_j = (A p_j)_i and x_j = x_{j-1} + alpha_{j-1} p_{j-1}
+// (x lags one phase), into the other buffer of each ping-pong pair (r: r | z, q: q | q1,
+// p: p0 | p1), so no CTA overwrites a value another CTA still gathers.  The barrier of
+// phase j reduces five partials: p_j.q_j (alpha_j), r_j.r_j (the criteria of iteration
+// j, exact), r_j.z_j (rz_j, exact) and z_j.q_j, q_j.M q_j, from which
+//     rz_{j+1} = sum M (r_j - alpha_j q_j)^2 = rz_j - 2 alpha_j z_j.q_j + alpha_j^2 q_j.M q_j
+// gives beta_j before r_{j+1} exists (no orthogonality is assumed: the identity is exact,
+// only its rounding differs from the direct dot, by a few ulps of rz_j; rz_{j+1} itself
+// is recomputed exactly at the next barrier for alpha_{j+1} and the breakdown test).
+// Per iteration: A + 9 V n bytes (gathered r, q, p, M; own x read; r, p, q, x stored)
+// instead of A + 12 V n, and one barrier instead of two.  The stop decision of iteration
+// j is taken after phase j, so the last phase's p, q are computed and discarded.
+// Stage of the single-sync kernel: the block's matrix ranges (StreamLayout) followed by
+// five own-row vector ranges [r0, r1) -- r_{j-1}, p_{j-1}, q_{j-1}, M, x -- all moved by
+// TMA one block ahead, so the own-row update never waits on global memory.
+template <class V, class I>
+struct Cg1Layout {
+    StreamLayout<V, I> L;
+    int cap_x;  // elements per vector range (R rows + alignment slack)
+    __host__ __device__ Cg1Layout(int R, int nnz_cap) : L(R, nnz_cap) { cap_x = (R + 2 * (16 / (int)sizeof(V)) + 3) & ~3; }
+    __host__ __device__ size_t vec_bytes() const { return ((size_t)cap_x * sizeof(V) + 15) & ~size_t(15); }
+    __host__ __device__ size_t off_x(int k) const { return L.stage_bytes() + (size_t)k * vec_bytes(); }
+    __host__ __device__ size_t stage_bytes() const { return off_x(5); }
+};
+
+template <class V, class I, int R, int MB>
+__global__ void __launch_bounds__(R, MB) cg1_persistent_kernel(CgPArgs a) {
+    // gathered out-of-block columns in flight per thread (four loads each)
+    constexpr int kGU = 4;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ StreamMeta meta[2];
+    __shared__ int64_t vbase[2];
+    Ctl *c = a.ctl;
+    if (c->done) return;  // setup found the exact solution
+    const I *rp = (const I *)a.rp, *ci = (const I *)a.ci;
+    const V *val = (const V *)a.val, *inv = (const V *)a.inv;
+    V *x = (V *)a.x;
+    const int64_t n = a.n, nnz = a.nnz;
+    const Cg1Layout<V, I> CL(R, a.nnz_cap);
+    const size_t sb = CL.stage_bytes();
+    const int tid = threadIdx.x;
+    const int G = gridDim.x;
+    const int64_t nblk = a.nblk, bq = a.bq, rem = a.rem;
+    const int64_t bid = blockIdx.x;
+    const uint64_t pol = policy_evict_first();
+    unsigned long long *count = &c->barrier;
+    unsigned long long epoch = 0;
+    // row-pointer bounds of this CTA's kb blocks, loaded once (issue() then starts its
+    // bulk copies without a dependent global load on the critical thread)
+    int64_t *kbnd = reinterpret_cast<int64_t *>(smem + 2 * sb);
+    for (int q = tid; q < a.kb; q += R) {
+        const int64_t blk = bid + (int64_t)q * G;
+        kbnd[2 * q] = rp[cg_block_row(blk, bq, rem)];
+        kbnd[2 * q + 1] = rp[min(cg_block_row(blk + 1, bq, rem), n)];
+    }
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    // stage block blk for phase jc into slot s (thread 0 only): matrix ranges + own-row
+    // vectors of phase jc (phase 0: r_0 and z_0 = p_0; phase jc > 0: r, p, q of jc - 1)
+    auto issue = [&](int64_t blk, int s, int64_t jc) {
+        unsigned char *st = smem + s * sb;
+        V *sv = reinterpret_cast<V *>(st);
+        I *sc = reinterpret_cast<I *>(st + CL.L.off_c());
+        I *sr = reinterpret_cast<I *>(st + CL.L.off_r());
+        const int64_t r0 = cg_block_row(blk, bq, rem), r1 = min(cg_block_row(blk + 1, bq, rem), n);
+        const int64_t q = (blk - bid) / G;
+        const int64_t k0 = kbnd[2 * q], k1 = kbnd[2 * q + 1];
+        StreamMeta m;
+        m.r0 = r0;
+        m.r1 = r1;
+        uint32_t bv = stage_range(val, k0, k1, nnz, sv, m.av);
+        uint32_t bc = stage_range(ci, k0, k1, nnz, sc, m.ac);
+        uint32_t br = stage_range(rp, r0, r1 + 1, n + 1, sr, m.ar);
+        const bool odd = jc & 1;
+        const V *src[5] = {(const V *)(jc == 0 ? a.r : odd ? a.r : a.z),
+                           (const V *)(jc == 0 ? a.z : odd ? a.p0 : a.p1),
+                           jc == 0 ? nullptr : (const V *)(odd ? a.q : a.q1), inv, x};
+        uint32_t bx[5];
+        int64_t base = r0;
+#pragma unroll
+        for (int k = 0; k < 5; ++k)
+            bx[k] = src[k] ? stage_range(src[k], r0, r1, n, reinterpret_cast<V *>(st + CL.off_x(k)), base) : 0;
+        meta[s] = m;
+        vbase[s] = base;
+        mbar_arrive_expect_tx(&bar[s], bv + bc + br + bx[0] + bx[1] + bx[2] + bx[3] + bx[4]);
+        if (bv) bulk_g2s(sv, val + m.av, bv, &bar[s], pol);
+        if (bc) bulk_g2s(sc, ci + m.ac, bc, &bar[s], pol);
+        if (br) bulk_g2s(sr, rp + m.ar, br, &bar[s], pol);
+#pragma unroll
+        for (int k = 0; k < 5; ++k)
+            if (bx[k]) bulk_g2s(reinterpret_cast<V *>(st + CL.off_x(k)), src[k] + base, bx[k], &bar[s]);
+    };
+    uint32_t seq = 0;
+    if (tid == 0 && bid < nblk) issue(bid, 0, 0);
+
+    const int64_t it0 = c->iter;
+    double rz = c->rz, alpha = 0.0, beta = 0.0;
+    bool bad_beta = false;  // rz_{j+1} expansion not finite: stop at the next barrier
+    const double bnorm = c->bnorm;
+    for (int64_t j = 0;; ++j) {
+        const bool first = j == 0;
+        const bool odd = j & 1;  // phase j writes buffer j & 1, reads the other
+        // r_0 in r; z holds z_0 for phase 0, then the odd r's
+        const V *rin = (const V *)(odd ? a.r : a.z), *qin = (const V *)(odd ? a.q : a.q1),
+                *pin = (const V *)(first ? a.z : odd ? a.p0 : a.p1);
+        V *rout = (V *)(odd ? a.z : a.r), *qout = (V *)(odd ? a.q1 : a.q), *pout = (V *)(odd ? a.p1 : a.p0);
+        double part[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // p.q, r.r, r.z, z.q, q.Mq
+        for (int64_t blk = bid; blk < nblk; blk += G, ++seq) {
+            const int s = seq & 1;
+            const bool wrap = blk + G >= nblk;  // next: this phase's next block or the next phase's first
+            // (a CTA owning one block stages its next-phase copy only after writing it)
+            const bool defer = wrap && blk == bid;
+            if (tid == 0 && !defer) issue(wrap ? bid : blk + G, s ^ 1, wrap ? j + 1 : j);
+            mbar_wait(&bar[s], (seq >> 1) & 1);
+            unsigned char *st = smem + s * sb;
+            const V *sv = reinterpret_cast<const V *>(st);
+            const I *sc = reinterpret_cast<const I *>(st + CL.L.off_c());
+            const I *sr = reinterpret_cast<const I *>(st + CL.L.off_r());
+            V *s_r = reinterpret_cast<V *>(st + CL.off_x(0));  // r_{j-1}, then z_j
+            V *s_p = reinterpret_cast<V *>(st + CL.off_x(1));  // p_{j-1}, then p_j
+            const V *s_q = reinterpret_cast<const V *>(st + CL.off_x(2));
+            const V *s_m = reinterpret_cast<const V *>(st + CL.off_x(3));
+            const V *s_x = reinterpret_cast<const V *>(st + CL.off_x(4));
+            const StreamMeta m = meta[s];
+            const int64_t vb = vbase[s];
+            const int64_t i = m.r0 + tid;
+            const int64_t nr = m.r1 - m.r0;
+            const bool own = i < m.r1;
+            const int64_t t = i - vb;
+            // own rows: r_j, z_j, p_j, x_j from the staged vectors; p_j replaces p_{j-1} in
+            // the stage (in-block gathers read it there), z_j replaces r_{j-1}
+            if (own) {
+                V ri, zi, pi;
+                if (first) {
+                    ri = s_r[t];
+                    zi = s_p[t];
+                    pi = zi;
+                } else {
+                    const V pp = s_p[t];
+                    ri = axpy_e(-alpha, s_q[t], s_r[t]);
+                    zi = inv ? vmul(ri, s_m[t]) : ri;
+                    pi = axpy_e(1.0, zi, scal_e(beta, pp));
+                    x[i] = axpy_e(alpha, pp, s_x[t]);
+                    rout[i] = ri;
+                }
+                pout[i] = pi;
+                s_p[t] = pi;
+                s_r[t] = zi;
+                part[1] = addd(part[1], mulp(ri, ri));
+                part[2] = addd(part[2], mulp(ri, zi));
+            }
+            __syncthreads();
+            if (own) {
+                const int64_t kb = sr[i - m.ar], ke = sr[i + 1 - m.ar];
+                double acc = 0.0;
+                for (int64_t k = kb; k < ke; k += kGU) {
+                    V vv[kGU], bb[kGU];
+#pragma unroll
+                    for (int u = 0; u < kGU; ++u) {
+                        const int64_t kk = k + u < ke ? k + u : ke - 1;
+                        const int64_t col = (int64_t)sc[kk - m.ac];
+                        vv[u] = sv[kk - m.av];
+                        const uint64_t off = (uint64_t)(col - m.r0);
+                        if (off < (uint64_t)nr) {
+                            bb[u] = s_p[col - vb];
+                        } else if (first) {
+                            bb[u] = pin[col];
+                        } else {  // p_j re-evaluated at an out-of-block column
+                            const V rc = axpy_e(-alpha, qin[col], rin[col]);
+                            const V zc = inv ? vmul(rc, inv[col]) : rc;
+                            bb[u] = axpy_e(1.0, zc, scal_e(beta, pin[col]));
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < kGU; ++u)
+                        if (k + u < ke) acc = addd(acc, mulp(vv[u], bb[u]));
+                }
+                const V qi = (V)acc;
+                qout[i] = qi;
+                const double di = inv ? (double)s_m[t] : 1.0;
+                part[0] = addd(part[0], mulp(s_p[t], qi));
+                part[3] = addd(part[3], __dmul_rn((double)s_r[t], (double)qi));
+                part[4] = addd(part[4], __dmul_rn(__dmul_rn((double)qi, di), (double)qi));
+            }
+            // the next phase stages r, p, q, x by TMA (async proxy): order this thread's
+            // generic stores before it, then release the stage
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            __syncthreads();
+            if (tid == 0 && defer) issue(bid, s ^ 1, j + 1);
+        }
+        double tot[5];
+        // partial slots ping-pong by epoch: a CTA that is one barrier ahead never
+        // overwrites the slots another CTA is still summing
+        ++epoch;
+        grid_allreduce<5, R>(part, a.partials + (epoch & 1) * 5 * G, count, epoch * G, tot);
+        const int64_t it = it0 + j;  // iterations completed: x_j, r_j
+        if (!first) {  // end of iteration j (solvers.py:207-216): criteria on ||r_j||
+            const double rnorm = sqrt(tot[1]);
+            int reason = check_criteria(c, it, rnorm, bnorm);
+            if (reason == STOP_NONE && rnorm == 0.0) reason = STOP_RESIDUAL;
+            if (bid == 0 && tid == 0) {
+                c->rnorm = rnorm;
+                record(c, it, rnorm);
+            }
+            if (reason != STOP_NONE) {
+                if (bid == 0 && tid == 0) finish_with(c, it, reason);
+                break;
+            }
+            if (!isfinite(tot[2]) || rz == 0.0 || bad_beta) {  // rz_new (solvers.py:217-222)
+                if (bid == 0 && tid == 0) breakdown(c, it);
+                break;
+            }
+            rz = tot[2];
+        }
+        // iteration j + 1 (solvers.py:202-206): alpha from p_j.q_j
+        const double pq = tot[0];
+        if (!isfinite(pq) || pq <= kBreakdownRtol * fabs(rz)) {
+            if (bid == 0 && tid == 0) breakdown(c, it + 1);
+            break;
+        }
+        alpha = rz / pq;
+        const double rz_next = rz - 2.0 * alpha * tot[3] + alpha * alpha * tot[4];
+        beta = rz_next / rz;
+        bad_beta = !isfinite(beta);  // (the phase still runs; its barrier reports the breakdown)
+    }
+    if (tid == 0 && bid < nblk) mbar_wait(&bar[seq & 1], (seq >> 1) & 1);  // drain the prefetch
+    if (bid == 0 && tid == 0) {
+        c->rz = rz;
+        c->beta = beta;
+        c->tphase[4] = G;
+    }
+}
+
 // max stored entries of any block of the balanced partition (the stage capacity)
 template <class I>
 __global__ void cg_block_nnz_max_kernel(const I *rp, int64_t n, int64_t nblk, int64_t bq, int64_t rem, unsigned long long *out) {
@@ -375,7 +631,7 @@ __global__ void cg_block_nnz_max_kernel(const I *rp, int64_t n, int64_t nblk, in
 static thread_local int g_cg_last_rows = 0;  // block rows of the last persistent launch
 
 template <class V, class I, int R>
-bool cg_persistent_launch_r(const sb_matrix &M, const CgPArgs &proto, cudaStream_t st, cudaError_t &err) {
+bool cg_persistent_launch_r(const sb_matrix &M, const CgPArgs &proto, bool single, cudaStream_t st, cudaError_t &err) {
     err = cudaSuccess;
     sb_csr A;
     if (M.format == SB_FMT_CSR) {
@@ -388,10 +644,14 @@ bool cg_persistent_launch_r(const sb_matrix &M, const CgPArgs &proto, cudaStream
         return false;
     }
     if (!A.plan || A.plan->kernel != SB_CSR_STREAM || A.rows == 0) return false;
-    auto kern = cg_persistent_kernel<V, I, R>;
+    // single-sync kernel: CTAs per SM from SPARSEB200_CG1_MB (threads per SM = MB R)
+    static const int mb_env = getenv("SPARSEB200_CG1_MB") ? atoi(getenv("SPARSEB200_CG1_MB")) : 0;
+    const int mb = (mb_env == 3 || mb_env == 4 ? mb_env : 3) * 256 / R;  // 3: 80 registers, 3 stages of 68 KB
+    auto kern = !single ? cg_persistent_kernel<V, I, R>
+                : mb * R == 768 ? cg1_persistent_kernel<V, I, R, 768 / R> : cg1_persistent_kernel<V, I, R, 1024 / R>;
     ensure_max_smem((const void *)kern);
     const int sms = device_info().sms;
-    const int per_sm = 1024 / R;
+    const int per_sm = single ? mb : 1024 / R;
     int64_t grid = (int64_t)per_sm * sms;
     const int64_t nb_min = ceil_div(A.rows, R);
     if (grid > nb_min) grid = nb_min;
@@ -410,7 +670,8 @@ bool cg_persistent_launch_r(const sb_matrix &M, const CgPArgs &proto, cudaStream
         return false;
     if (hmax > (1u << 20)) return false;
     const int cap = (int)((hmax + 63) & ~63ull);
-    const size_t smem = 2 * StreamLayout<V, I>(R, cap > 0 ? cap : 64).stage_bytes();
+    const size_t smem = single ? 2 * Cg1Layout<V, I>(R, cap > 0 ? cap : 64).stage_bytes() + 16 * kb
+                               : 2 * StreamLayout<V, I>(R, cap > 0 ? cap : 64).stage_bytes() + 16 * kb;
     if (smem > 220 * 1024) return false;
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, R, smem) != cudaSuccess || occ < per_sm) {
@@ -455,9 +716,10 @@ bool cg_persistent_launch(const sb_matrix &M, const CgPArgs &proto, cudaStream_t
     const int64_t rows = M.format == SB_FMT_CSR ? ((const sb_csr *)M.mat)->rows
                                                 : (M.format == SB_FMT_COO ? ((const sb_coo *)M.mat)->rows : 0);
     const int r = r_env ? r_env : (rows <= (int64_t(1) << 20) ? 512 : 256);
-    if (r == 512 && cg_persistent_launch_r<V, I, 512>(M, proto, st, err)) return true;
+    const bool single = proto.q1 != nullptr;
+    if (r == 512 && cg_persistent_launch_r<V, I, 512>(M, proto, single, st, err)) return true;
     if (err != cudaSuccess) return false;
-    return cg_persistent_launch_r<V, I, 256>(M, proto, st, err);
+    return cg_persistent_launch_r<V, I, 256>(M, proto, single, st, err);
 }
 
 // CG loop shape: 3 = persistent kernel where applicable (default), else the graph loop
@@ -471,6 +733,12 @@ static std::atomic<int> g_cg_mode{[] {
     return e ? atoi(e) : 3;
 }()};
 constexpr size_t kPersistentMaxVectorBytes = 24u << 20;
+// grid barriers per persistent CG iteration: 2 = the two-barrier kernel (default), 1 = the
+// single-sync kernel (SPARSEB200_CG_SYNC=1; measured slower, profiles/README.md round 2)
+static std::atomic<int> g_cg_sync{[] {
+    const char *e = getenv("SPARSEB200_CG_SYNC");
+    return e && atoi(e) == 1 ? 1 : 2;
+}()};
 static thread_local int g_cg_last_loop = -1;  // loop shape of this thread's last CG solve
 
 // ---------------------------------------------------------------- CG with ILU / IC factors
@@ -630,7 +898,7 @@ sb_status cg_solve(const SolveArgs &a) {
     const int64_t cap = a.log->history_cap;
     SolverWs w = carve_ws(a.ws, SB_SOLVER_CG, sizeof(V), n, 0, cap);
     V *r = ws_vec<V>(w, 0), *z = ws_vec<V>(w, 1), *p = ws_vec<V>(w, 2), *q = ws_vec<V>(w, 3),
-      *t = ws_vec<V>(w, 4);
+      *t = ws_vec<V>(w, 4), *q1 = ws_vec<V>(w, 5);
     const V *b = (const V *)a.b->data, *inv = (const V *)a.inv;
     V *x = (V *)a.x->data;
     Ctl *ctl = w.ctl;
@@ -663,16 +931,20 @@ sb_status cg_solve(const SolveArgs &a) {
         pa.prof = prof ? reinterpret_cast<unsigned long long *>(part + 4096) : nullptr;  // G <= 1000
         static const int pf = getenv("SPARSEB200_CG_PF") ? atoi(getenv("SPARSEB200_CG_PF")) : 1;
         pa.pf = pf;
+        pa.q1 = g_cg_sync.load() == 1 ? q1 : nullptr;  // single-sync kernel (opt-in)
         cudaError_t le;
         if (cg_persistent_launch<V, I>(M, pa, a.st, le)) {
             g_cg_last_loop = 3;
             SB_CUDA(cudaMemcpyAsync(&h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, a.st));
             SB_CUDA(cudaStreamSynchronize(a.st));
-            if (prof && h.iter > 0)
+            if (prof && h.iter > 0 && pa.q1)
+                fprintf(stderr, "[sparseb200] single-sync persistent CG %lld it: phase %.2f | barrier %.2f us/it\n",
+                        (long long)h.iter, h.tphase[0] * 1e-3 / h.iter, h.tphase[1] * 1e-3 / h.iter);
+            else if (prof && h.iter > 0)
                 fprintf(stderr, "[sparseb200] persistent CG %lld it: A %.2f | bar1 %.2f | B %.2f | bar2 %.2f us/it\n",
                         (long long)h.iter, h.tphase[0] * 1e-3 / h.iter, h.tphase[1] * 1e-3 / h.iter,
                         h.tphase[2] * 1e-3 / h.iter, h.tphase[3] * 1e-3 / h.iter);
-            if (prof && h.iter > 14) {  // per barrier: arrival spread, CTA-0 wait, wake-up
+            if (prof && h.iter > 14 && !pa.q1) {  // per barrier: arrival spread, CTA-0 wait, wake-up
                 const int G = (int)h.tphase[4];
                 std::vector<unsigned long long> st(20 * (size_t)G);
                 SB_CUDA(cudaMemcpy(st.data(), pa.prof, st.size() * 8, cudaMemcpyDeviceToHost));
@@ -747,6 +1019,7 @@ using namespace sb;
 extern "C" {
 
 void sb_set_cg_fused(int mode) { g_cg_mode = mode; }
+void sb_set_cg_sync(int barriers) { g_cg_sync = barriers == 1 ? 1 : 2; }
 int sb_cg_last_loop(void) { return g_cg_last_loop; }
 int sb_cg_last_block_rows(void) { return g_cg_last_loop == 3 ? g_cg_last_rows : 0; }
 

@@ -148,6 +148,14 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         : "memory");
 }
 
+// the same without an L2 eviction hint (vectors that are re-read soon)
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+
 // ------------------------------------------------------------------ programmatic dependent launch
 // Kernels launched with launch_pdl() may start while their predecessor on the stream is
 // still draining: everything before pdl_wait() must touch only data no predecessor

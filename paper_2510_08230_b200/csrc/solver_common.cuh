@@ -281,7 +281,7 @@ inline size_t a256(size_t b) { return (b + 255) & ~size_t(255); }
 
 inline int solver_num_vectors(int solver, int64_t dim) {
     switch (solver) {
-    case SB_SOLVER_CG: return 5;
+    case SB_SOLVER_CG: return 6;  // r z p q t + q1 (single-sync persistent loop)
     case SB_SOLVER_CGS: return 10;
     case SB_SOLVER_BICGSTAB: return 8;
     default: return (int)dim + 1 + 4;  // basis + r, t, z, w

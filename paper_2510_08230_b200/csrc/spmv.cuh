@@ -187,13 +187,19 @@ __global__ void __launch_bounds__(R, epi_min_ctas<Epi>(R)) csr_stream_kernel(int
     }
     __syncthreads();
 
-    auto issue = [&](int64_t blk, int s) {  // thread 0 only
+    // the row-pointer bounds of a block are loaded one block before its issue (thread 0
+    // would otherwise start every block one L2 round trip behind the other threads)
+    auto bounds = [&](int64_t blk, int64_t &k0, int64_t &k1) {
+        const int64_t r0 = blk * R, r1 = r0 + R < rows ? r0 + R : rows;
+        k0 = rp[r0];
+        k1 = rp[r1];
+    };
+    auto issue = [&](int64_t blk, int s, int64_t k0, int64_t k1) {  // thread 0 only
         unsigned char *st = smem + s * sb;
         V *sv = reinterpret_cast<V *>(st);
         I *sc = reinterpret_cast<I *>(st + L.off_c());
         I *sr = reinterpret_cast<I *>(st + L.off_r());
         const int64_t r0 = blk * R, r1 = r0 + R < rows ? r0 + R : rows;
-        const int64_t k0 = rp[r0], k1 = rp[r1];
         StreamMeta m;
         m.r0 = r0;
         m.r1 = r1;
@@ -210,9 +216,15 @@ __global__ void __launch_bounds__(R, epi_min_ctas<Epi>(R)) csr_stream_kernel(int
     // the first block's matrix ranges are immutable: their TMA copies are issued before
     // waiting on the predecessor kernel (programmatic dependent launch)
     int64_t blk = blockIdx.x;
-    if (tid == 0)
+    int64_t nk0 = 0, nk1 = 0;  // bounds of the next block to issue (thread 0)
+    if (tid == 0) {
         for (int q = 0; q < NS - 1; ++q)
-            if (blk + (int64_t)q * gridDim.x < nblk) issue(blk + (int64_t)q * gridDim.x, q);
+            if (blk + (int64_t)q * gridDim.x < nblk) {
+                bounds(blk + (int64_t)q * gridDim.x, nk0, nk1);
+                issue(blk + (int64_t)q * gridDim.x, q, nk0, nk1);
+            }
+        if (blk + (int64_t)(NS - 1) * gridDim.x < nblk) bounds(blk + (int64_t)(NS - 1) * gridDim.x, nk0, nk1);
+    }
     pdl_wait();
     pdl_trigger();
     if (epi.skip()) {
@@ -226,8 +238,11 @@ __global__ void __launch_bounds__(R, epi_min_ctas<Epi>(R)) csr_stream_kernel(int
     for (int it = 0; blk < nblk; blk += gridDim.x, ++it) {
         const int s = it % NS;
         const uint32_t parity = (it / NS) & 1;
-        if (tid == 0 && blk + (int64_t)(NS - 1) * gridDim.x < nblk)
-            issue(blk + (int64_t)(NS - 1) * gridDim.x, (it + NS - 1) % NS);
+        if (tid == 0 && blk + (int64_t)(NS - 1) * gridDim.x < nblk) {
+            const int64_t bi = blk + (int64_t)(NS - 1) * gridDim.x;
+            issue(bi, (it + NS - 1) % NS, nk0, nk1);
+            if (bi + gridDim.x < nblk) bounds(bi + gridDim.x, nk0, nk1);
+        }
         mbar_wait(&bar[s], parity);
         const unsigned char *st = smem + s * sb;
         const V *sv = reinterpret_cast<const V *>(st);

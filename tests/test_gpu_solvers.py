@@ -269,26 +269,32 @@ def test_cg_persistent_kernel(dev, dtype):
     inv = sbref.jacobi_create(rp, ci, v)[0]
     rtol = 1e-9 if dtype == np.float64 else 1e-4
     set_mode = _lib.fn("sb_set_cg_fused")
+    set_sync = _lib.fn("sb_set_cg_sync")
     try:
         for crit, pre, xi, its, rf in (([sp.Iteration(5000), sp.ResidualNorm(1e-7)], True, None, 5000, 1e-7),
                                        ([sp.Iteration(7)], True, x0, 7, None),
                                        ([sp.Iteration(8)], False, x0, 8, None),
                                        ([sp.Iteration(5000), sp.ResidualNorm(1e-6)], False, None, 5000, 1e-6)):
             logs = {}
-            for mode in (1, 3):
-                set_mode(mode)
+            for mode in (1, 3, 4):  # 3: two-barrier persistent kernel, 4: single-sync kernel
+                set_mode(min(mode, 3))
+                set_sync(1 if mode == 4 else 2)
                 logs[mode] = solve(dev, "cg", a, b, crit, precond=sp.jacobi_create(a) if pre else False, x0=xi)
+                assert _lib.fn("sb_cg_last_loop")() == min(mode, 3)
+            set_sync(2)
             ref, xr = sbref.solve("cg", rp, ci, v, b, x0=xi, inv_diag=inv if pre else None, max_iters=its,
                                   reduction_factor=rf)
-            (l1, x1, _), (l3, x3, _) = logs[1], logs[3]
-            assert l3.iterations == l1.iterations or (rf and within(l3.iterations, ref.iterations))
-            assert l3.stop_reason == l1.stop_reason == ref.stop_reason
-            n = min(5, len(ref.residual_history))
-            np.testing.assert_allclose(l3.residual_history[:n], ref.residual_history[:n], rtol=rtol)
-            if rf is None:
-                np.testing.assert_allclose(x3, x1, rtol=rtol * 10, atol=rtol)
-            else:
-                assert l3.residual_history[-1] <= rf * np.linalg.norm(b.astype(np.float64)) * 1.0001
+            l1, x1, _ = logs[1]
+            for m3 in (3, 4):
+                l3, x3, _ = logs[m3]
+                assert l3.iterations == l1.iterations or (rf and within(l3.iterations, ref.iterations))
+                assert l3.stop_reason == l1.stop_reason == ref.stop_reason
+                n = min(5, len(ref.residual_history))
+                np.testing.assert_allclose(l3.residual_history[:n], ref.residual_history[:n], rtol=rtol)
+                if rf is None:
+                    np.testing.assert_allclose(x3, x1, rtol=rtol * 10, atol=rtol)
+                else:
+                    assert l3.residual_history[-1] <= rf * np.linalg.norm(b.astype(np.float64)) * 1.0001
         set_mode(3)
         if dtype == np.float64:
             zero = sp.csr_from_dense(dev, np.zeros((300, 300)), keep_zeros=False).with_kernel("stream")
