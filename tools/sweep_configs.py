@@ -59,6 +59,8 @@ def fmt_bytes(mat, vb, ib):
     if isinstance(mat, sp.CsrMatrix):
         return (vb + ib) * mat.nnz + ib * (n + 1) + 2 * vb * n
     if isinstance(mat, sp.CooMatrix):
+        if mat.kernel_request == "auto":  # row-pointer index + CSR kernels: row_idxs never read
+            return (vb + ib) * mat.nnz + ib * (n + 1) + 2 * vb * n
         return (vb + 2 * ib) * mat.nnz + 2 * vb * n
     if isinstance(mat, sp.SellpMatrix):
         return (vb + ib) * mat.stored + ib * (2 * mat.num_slices + 1) + 2 * vb * n
