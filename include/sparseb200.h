@@ -154,6 +154,14 @@ typedef struct {
     const void *slice_lengths, *slice_sets, *col_idxs, *values;
     int64_t max_block_entries;
     const void *row_perm;
+    /* split plan (optional, staged kernel only; NULL = every block is one work item):
+     * int64 [first piece of each block (nblk + 1) | block of each piece (num_pieces) |
+     * blocks of more than one piece (num_split)], nblk = ceil(num_slices / (128 / S));
+     * a piece is at most piece_entries stored entries of its block; carry holds
+     * num_pieces x 128 doubles (partial row sums of split blocks, summed in piece order). */
+    const void *piece_plan;
+    int64_t num_pieces, num_split, piece_entries;
+    void *carry;
 } sb_sellp;
 
 /* Hybrid(w): the first min(len_i, w) entries of each row in ELL(w), the rest in COO */

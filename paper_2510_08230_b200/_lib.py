@@ -72,7 +72,9 @@ class SbEll(ctypes.Structure):
 class SbSellp(ctypes.Structure):
     _fields_ = [("rows", c_i64), ("cols", c_i64), ("slice_size", c_i64), ("num_slices", c_i64),
                 ("slice_lengths", c_vp), ("slice_sets", c_vp), ("col_idxs", c_vp),
-                ("values", c_vp), ("max_block_entries", c_i64), ("row_perm", c_vp)]
+                ("values", c_vp), ("max_block_entries", c_i64), ("row_perm", c_vp),
+                ("piece_plan", c_vp), ("num_pieces", c_i64), ("num_split", c_i64),
+                ("piece_entries", c_i64), ("carry", c_vp)]
 
 
 class SbHybrid(ctypes.Structure):

@@ -229,7 +229,8 @@ std::string matrix_key(const sb_matrix &M) {
         const sb_sellp &A = *(const sb_sellp *)M.mat;
         // max_block_entries picks block vs chunk kernel and sets the staged capacity
         // baked into the captured launch, so it is part of the key
-        s += ptr_key({A.slice_lengths, A.slice_sets, A.col_idxs, A.values, A.row_perm}) + std::to_string(A.rows) +
+        s += ptr_key({A.slice_lengths, A.slice_sets, A.col_idxs, A.values, A.row_perm, A.piece_plan, A.carry}) +
+             std::to_string(A.num_pieces) + "," + std::to_string(A.piece_entries) + "," + std::to_string(A.rows) +
              "," + std::to_string(A.slice_size) + "," + std::to_string(A.num_slices) + "," +
              std::to_string(A.max_block_entries);
         break;

@@ -1429,6 +1429,155 @@ __global__ void __launch_bounds__(128) sellp_chunk_kernel(int64_t rows, int64_t 
     epi.finish(part);
 }
 
+// ------------------------------------------------------------ SELL-P: split pieces
+// Load balance for blocks far larger than the average (power-law rows, SELL-C-sigma
+// windows that gather the longest rows): every block's entry range [lo, hi) is cut into
+// pieces of at most `pe` entries (whole chunks), a piece is one work item of a grid-stride
+// loop, and the chunks of a piece stream through the same TMA ring as sellp_chunk_kernel.
+// A block of one piece stores its rows directly (bit-exact, the stored order); a split
+// block's pieces leave one partial sum per row in `carry` (slot = piece index), and
+// sellp_piece_fixup_kernel adds them in piece order.  Plan (int64, built by the
+// frontend): pstart[nblk + 1] (first piece of each block), pblock[npieces] (block of each
+// piece), split[nsplit] (blocks of more than one piece).
+template <class V, class I, int S>
+__global__ void __launch_bounds__(128) sellp_piece_kernel(int64_t rows, int64_t nslices,
+                                                           const I *__restrict__ sl,
+                                                           const I *__restrict__ ss,
+                                                           const I *__restrict__ col,
+                                                           const V *__restrict__ val,
+                                                           const V *__restrict__ b, int64_t ldb,
+                                                           int cap_entries, const int64_t *__restrict__ plan,
+                                                           int64_t npieces, int64_t pe, double *carry,
+                                                           V *x, int64_t ldx, const I *__restrict__ perm) {
+    constexpr int SPB = 128 / S;
+    static_assert(SPB >= 1 && SPB <= 4, "slice size 32, 64 or 128");
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ SellpMeta meta[2];
+    __shared__ int32_t split_of[2];  // the staged chunk's piece belongs to a split block
+    constexpr int VV = 16 / sizeof(V), VI = 16 / sizeof(I);
+    const size_t cap_v = (size_t)cap_entries + 2 * VV, cap_c = (size_t)cap_entries + 2 * VI;
+    const size_t off_c = (cap_v * sizeof(V) + 15) & ~size_t(15);
+    const size_t stage_bytes = (off_c + cap_c * sizeof(I) + 15) & ~size_t(15);
+    const int64_t chunk = (int64_t)(cap_entries / S) * S;
+    const int tid = threadIdx.x;
+    const int64_t nblk = (nslices + SPB - 1) / SPB;
+    const int64_t total = (int64_t)ss[nslices] * S;
+    const int64_t *pstart = plan, *pblock = plan + nblk + 1;
+    const uint64_t pol = policy_evict_first();
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    // thread 0: stage chunk [clo, min(clo + chunk, piece end)) of piece pc; true if it
+    // was the piece's last chunk, else clo advances to the next chunk
+    auto issue = [&](int64_t pc, int64_t &clo, int st) -> bool {
+        unsigned char *p = smem + st * stage_bytes;
+        V *sv = reinterpret_cast<V *>(p);
+        I *sc = reinterpret_cast<I *>(p + off_c);
+        const int64_t blk = pblock[pc], q = pc - pstart[blk];
+        const int64_t s0 = blk * SPB, s1 = s0 + SPB < nslices ? s0 + SPB : nslices;
+        const int64_t lo = (int64_t)ss[s0] * S, hi = (int64_t)ss[s1] * S;
+        const int64_t plo = lo + q * pe, phi = plo + pe < hi ? plo + pe : hi;
+        if (clo < plo) clo = plo;
+        const int64_t chi = clo + chunk < phi ? clo + chunk : phi;
+        SellpMeta m;
+        m.s0 = s0;
+        m.lo = lo;
+        m.clo = clo;
+        m.chi = chi;
+        m.last = chi == phi;
+        const uint32_t bv = stage_range(val, clo, chi, total, sv, m.bv);
+        const uint32_t bc = stage_range(col, clo, chi, total, sc, m.bc);
+        for (int j = 0; j < SPB; ++j) {
+            const int64_t s = s0 + j;
+            m.len[j] = s < s1 ? (int32_t)sl[s] : 0;
+            m.off[j] = s < s1 ? (int32_t)((int64_t)ss[s] * S - lo) : 0;
+        }
+        meta[st] = m;
+        split_of[st] = pstart[blk + 1] - pstart[blk] > 1;
+        mbar_arrive_expect_tx(&bar[st], bv + bc);
+        if (bv) bulk_g2s(sv, val + m.bv, bv, &bar[st], pol);
+        if (bc) bulk_g2s(sc, col + m.bc, bc, &bar[st], pol);
+        clo = chi;
+        return chi == phi;
+    };
+    int64_t pc = blockIdx.x;
+    int64_t npc = pc, nclo = -1;
+    if (tid == 0 && pc < npieces && issue(pc, nclo, 0)) {
+        npc = pc + gridDim.x;
+        nclo = -1;
+    }
+    double acc = 0.0;
+    for (int it = 0; pc < npieces; ++it) {
+        const int st = it & 1;
+        const uint32_t parity = (it >> 1) & 1;
+        if (tid == 0 && npc < npieces && issue(npc, nclo, st ^ 1)) {
+            npc += gridDim.x;
+            nclo = -1;
+        }
+        mbar_wait(&bar[st], parity);
+        const unsigned char *p = smem + st * stage_bytes;
+        const V *sv = reinterpret_cast<const V *>(p);
+        const I *sc = reinterpret_cast<const I *>(p + off_c);
+        const SellpMeta &m = meta[st];
+        const int j = tid / S, l = tid % S;
+        const int64_t i = (m.s0 + j) * S + l;
+        const bool last = m.last;
+        if (j < SPB && i < rows) {
+            const int len = m.len[j];
+            const int64_t lo = m.lo, off = m.off[j];
+            const int64_t rel0 = m.clo - lo - off, rel1 = m.chi - lo - off;
+            int k = rel0 > 0 ? (int)(rel0 / S) : 0;
+            const int kend = rel1 <= 0 ? 0 : (int)(rel1 / S < len ? rel1 / S : len);
+            const int64_t ov = lo + off + l - m.bv, oc = lo + off + l - m.bc;
+            for (; k < kend; k += 8) {
+                V vv[8], bb[8];
+                I cc[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int kk = k + u < kend ? k + u : kend - 1;
+                    vv[u] = sv[ov + (int64_t)kk * S];
+                    cc[u] = k + u < kend ? sc[oc + (int64_t)kk * S] : (I)-1;
+                    bb[u] = cc[u] >= 0 ? __ldg(b + (int64_t)cc[u] * ldb) : (V)0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (cc[u] >= 0) acc = addd(acc, mulp(vv[u], bb[u]));
+            }
+        }
+        if (last) {
+            if (split_of[st])
+                carry[pc * 128 + tid] = acc;  // every thread: rows past the end stay unread
+            else if (j < SPB && i < rows)
+                x[(perm ? (int64_t)perm[i] : i) * ldx] = (V)acc;
+            acc = 0.0;
+            pc += gridDim.x;
+        }
+        __syncthreads();  // stage st consumed before it is re-issued
+    }
+}
+
+// rows of split blocks: the pieces' partial sums in piece order
+template <class V, class I, int S>
+__global__ void __launch_bounds__(128) sellp_piece_fixup_kernel(int64_t rows, int64_t nslices, const int64_t *__restrict__ plan,
+                                                                 int64_t npieces, int64_t nsplit, const double *__restrict__ carry,
+                                                                 V *x, int64_t ldx, const I *__restrict__ perm) {
+    constexpr int SPB = 128 / S;
+    const int64_t nblk = (nslices + SPB - 1) / SPB;
+    const int64_t *pstart = plan, *split = plan + nblk + 1 + npieces;
+    for (int64_t q = blockIdx.x; q < nsplit; q += gridDim.x) {
+        const int64_t blk = split[q];
+        const int64_t i = blk * 128 + threadIdx.x;  // = (blk SPB + j) S + l
+        if (i >= rows) continue;
+        double acc = 0.0;
+        for (int64_t pc = pstart[blk]; pc < pstart[blk + 1]; ++pc) acc = addd(acc, carry[pc * 128 + threadIdx.x]);
+        x[(perm ? (int64_t)perm[i] : i) * ldx] = (V)acc;
+    }
+}
+
 // Row-owned epilogue applied after a row-splitting SpMV (merge / COO / Hybrid):
 // re-reads x and feeds it to the epilogue (so fused dots work for every format).
 template <class V, class Epi>

@@ -357,9 +357,50 @@ cudaError_t launch_sellp_stream(const sb_sellp &A, const V *b, int64_t ldb, cons
     return cudaGetLastError();
 }
 
+// split-piece SELL-P (the plan's blocks cut into pieces; raw row sums into x_out)
+template <class V, class I, int S>
+cudaError_t launch_sellp_pieces(const sb_sellp &A, const V *b, int64_t ldb, V *x_out, int64_t ldx, cudaStream_t st) {
+    constexpr int VV = 16 / sizeof(V), VI = 16 / sizeof(I);
+    const int cap = (int)std::min<int64_t>(A.max_block_entries, std::max<int64_t>(2048 / S * S, S));
+    const size_t cap_v = (size_t)cap + 2 * VV, cap_c = (size_t)cap + 2 * VI;
+    const size_t off_c = (cap_v * sizeof(V) + 15) & ~size_t(15);
+    const size_t stage = (off_c + cap_c * sizeof(I) + 15) & ~size_t(15);
+    if (A.piece_entries <= 0 || A.piece_entries % (cap / S * S) != 0) return cudaErrorInvalidValue;
+    auto kern = sellp_piece_kernel<V, I, S>;
+    ensure_max_smem((const void *)kern);
+    int grid = persistent_grid(kern, 128, 2 * stage);
+    if (grid > A.num_pieces) grid = (int)A.num_pieces;
+    kern<<<grid, 128, 2 * stage, st>>>(A.rows, A.num_slices, (const I *)A.slice_lengths, (const I *)A.slice_sets,
+                                       (const I *)A.col_idxs, (const V *)A.values, b, ldb, cap,
+                                       (const int64_t *)A.piece_plan, A.num_pieces, A.piece_entries,
+                                       (double *)A.carry, x_out, ldx, (const I *)A.row_perm);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || A.num_split == 0) return e;
+    const int fg = (int)std::min<int64_t>(A.num_split, 148 * 16);
+    sellp_piece_fixup_kernel<V, I, S><<<fg, 128, 0, st>>>(A.rows, A.num_slices, (const int64_t *)A.piece_plan,
+                                                          A.num_pieces, A.num_split, (const double *)A.carry,
+                                                          x_out, ldx, (const I *)A.row_perm);
+    return cudaGetLastError();
+}
+
+inline bool sellp_split(const sb_sellp &A) {
+    return A.piece_plan && A.carry && A.num_pieces > 0 && A.max_block_entries > 0 &&
+           (A.slice_size == 32 || A.slice_size == 64 || A.slice_size == 128);
+}
+
 template <class V, class I, class Epi>
-cudaError_t sellp_apply(const sb_sellp &A, const V *b, int64_t ldb, const Epi &epi, cudaStream_t st) {
+cudaError_t sellp_apply(const sb_sellp &A, const V *b, int64_t ldb, V *x_out, int64_t ldx, const Epi &epi,
+                        cudaStream_t st) {
     if (A.rows == 0) return cudaSuccess;
+    if (sellp_split(A) && ((uintptr_t)A.values % 16 == 0) && ((uintptr_t)A.col_idxs % 16 == 0)) {
+        // row-splitting: raw sums first, the epilogue (if any) as a pass over x
+        if constexpr (epi_has_gather<Epi>::value) return cudaErrorNotSupported;
+        cudaError_t e = A.slice_size == 64   ? launch_sellp_pieces<V, I, 64>(A, b, ldb, x_out, ldx, st)
+                        : A.slice_size == 32 ? launch_sellp_pieces<V, I, 32>(A, b, ldb, x_out, ldx, st)
+                                             : launch_sellp_pieces<V, I, 128>(A, b, ldb, x_out, ldx, st);
+        if (e != cudaSuccess || is_plain_store<Epi>::value) return e;
+        return launch_epilogue_pass<V, I>(A.rows, x_out, ldx, epi, st);
+    }
     const bool staged = A.max_block_entries > 0 &&
                         ((uintptr_t)A.values % 16 == 0) && ((uintptr_t)A.col_idxs % 16 == 0) &&
                         (A.slice_size == 32 || A.slice_size == 64 || A.slice_size == 128);
@@ -414,7 +455,7 @@ cudaError_t matrix_apply(const sb_matrix &M, const V *b, int64_t ldb, V *x_out, 
     case SB_FMT_CSR: return csr_apply<V, I>(*(const sb_csr *)M.mat, b, ldb, x_out, ldx, epi, st);
     case SB_FMT_COO: return coo_apply<V, I>(*(const sb_coo *)M.mat, b, ldb, x_out, ldx, epi, st);
     case SB_FMT_ELL: return ell_apply<V, I>(*(const sb_ell *)M.mat, b, ldb, epi, st);
-    case SB_FMT_SELLP: return sellp_apply<V, I>(*(const sb_sellp *)M.mat, b, ldb, epi, st);
+    case SB_FMT_SELLP: return sellp_apply<V, I>(*(const sb_sellp *)M.mat, b, ldb, x_out, ldx, epi, st);
     case SB_FMT_HYBRID:
         return hybrid_apply<V, I>(*(const sb_hybrid *)M.mat, b, ldb, x_out, ldx, epi, st);
     default: return cudaErrorInvalidValue;
@@ -434,8 +475,8 @@ inline bool matrix_row_owning(const sb_matrix &M) {
         return A.plan && A.plan->row_ptrs && A.plan->csr_plan &&
                A.plan->csr_plan->kernel != SB_CSR_MERGE && A.plan->csr_plan->kernel != SB_CSR_TILE;
     }
-    case SB_FMT_ELL:
-    case SB_FMT_SELLP: return true;
+    case SB_FMT_ELL: return true;
+    case SB_FMT_SELLP: return !sellp_split(*(const sb_sellp *)M.mat);
     default: return false;
     }
 }

@@ -362,6 +362,7 @@ class SellpMatrix(_SparseBase):
         self._nnz = int((self.col_idxs >= 0).sum()) if nnz is None else int(nnz)
         self.max_block_entries = self._block_entries()
         self.staged = True  # TMA-staged slice kernel when the block fits shared memory
+        self._pieces = self._piece_plan()
 
     def with_staging(self, staged: bool) -> "SellpMatrix":
         """Same arrays (shared), staged (TMA) or direct SpMV kernel."""
@@ -369,6 +370,7 @@ class SellpMatrix(_SparseBase):
                         self.slice_sets, self.col_idxs, self.values, nnz=self._nnz,
                         row_perm=self.row_perm)
         m.staged = staged
+        m._pieces = self._pieces
         return m
 
     def _block_entries(self) -> int:
@@ -383,12 +385,43 @@ class SellpMatrix(_SparseBase):
         hi = torch.clamp(idx + spb, max=self.num_slices)
         return int(((ss[hi] - ss[idx]) * S).max())
 
+    def _piece_plan(self):
+        """Split plan of the staged kernel (csrc/spmv.cuh sellp_piece_kernel): blocks of
+        128 / S slices larger than one piece (a balanced share of all stored entries, at
+        least 8 TMA chunks) are cut into pieces whose partial row sums are added in piece
+        order.  None when no block exceeds one piece (the whole-block kernels run)."""
+        S = self.slice_size
+        if S not in (32, 64, 128) or self.num_slices == 0 or self.max_block_entries == 0:
+            return None
+        spb = 128 // S
+        chunk = min(self.max_block_entries, max(2048 // S * S, S)) // S * S
+        ss = self.slice_sets.long()
+        idx = torch.arange(0, self.num_slices, spb, device=ss.device)
+        ent = (ss[torch.clamp(idx + spb, max=self.num_slices)] - ss[idx]) * S
+        sms = torch.cuda.get_device_properties(ss.device).multi_processor_count
+        pe = max(8 * chunk, -(-int(ent.sum()) // (sms * 32)))
+        pe = -(-pe // chunk) * chunk
+        npb = torch.clamp((ent + pe - 1) // pe, min=1)
+        if int(npb.max()) <= 1:
+            return None
+        pstart = torch.zeros(idx.numel() + 1, dtype=torch.int64, device=ss.device)
+        pstart[1:] = torch.cumsum(npb, 0)
+        pblock = torch.repeat_interleave(torch.arange(idx.numel(), device=ss.device), npb)
+        split = torch.nonzero(npb > 1).flatten()
+        plan = torch.cat([pstart, pblock, split]).to(torch.int64).contiguous()
+        npieces = int(pstart[-1])
+        carry = torch.empty(npieces * 128, dtype=torch.float64, device=ss.device)
+        return plan, npieces, int(split.numel()), pe, carry
+
     def struct(self) -> _lib.SbSellp:
+        pc = self._pieces if self.staged else None
         return _lib.SbSellp(self.rows, self.cols, self.slice_size, self.num_slices,
                             _ptr(self.slice_lengths).value, _ptr(self.slice_sets).value,
                             _ptr(self.col_idxs).value, _ptr(self.values).value,
                             self.max_block_entries if self.staged else 0,
-                            _ptr(self.row_perm).value if self.row_perm is not None else None)
+                            _ptr(self.row_perm).value if self.row_perm is not None else None,
+                            _ptr(pc[0]).value if pc else None, pc[1] if pc else 0, pc[2] if pc else 0,
+                            pc[3] if pc else 0, _ptr(pc[4]).value if pc else None)
 
     @property
     def stored(self) -> int:

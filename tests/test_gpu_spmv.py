@@ -284,3 +284,60 @@ def test_stream_spmm_multi_rhs_bitwise(dev):
                 y = out(dev, n, vdt)
                 a.apply(vec(dev, bm[:, j]), y)
                 np.testing.assert_array_equal(got[:, j], host(y), err_msg=f"k={k} col={j}")
+
+
+@pytest.mark.parametrize("vdt", [np.float64, np.float32])
+def test_sellp_split_pieces(dev, vdt):
+    """SELL-P / SELL-C-sigma blocks far above the average size are cut into pieces
+    (sellp_piece_kernel + in-order fix-up): results against the oracle's CSR SpMV within
+    the fp tolerance, unsplit blocks bitwise equal to the whole-block kernel, and a CG
+    solve through the split operator (row-splitting epilogue pass) matches the CSR run."""
+    rng = np.random.default_rng(5)
+    n = 40000
+    lens = rng.integers(1, 8, n)
+    lens[rng.choice(n, 40, replace=False)] = rng.integers(3000, 12000, 40)
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    ci = np.concatenate([np.sort(rng.choice(n, k, replace=False)) for k in lens]).astype(np.int32)
+    v = rng.standard_normal(rp[-1]).astype(vdt)
+    a = csr(dev, rp, ci, v)
+    bv = rng.random(n).astype(vdt)
+    ref = sbref.csr_spmv(rp, ci, v, bv, threads=8)
+    x_whole = out(dev, n, vdt)
+    for mat in (sp.sellp_from_csr(a, 64), sp.sellp_from_csr(a, 32), sp.sellp_from_csr(a, 64, sigma=1024)):
+        assert mat._pieces is not None and mat._pieces[2] > 0  # some blocks are split
+        x = out(dev, n, vdt)
+        mat.apply(vec(dev, bv), x)
+        assert_close(host(x), ref, rp, v, bv)
+        # rows of unsplit blocks: bitwise what the whole-block kernel stores
+        whole = sp.SellpMatrix(dev, mat.rows, mat.cols, mat.slice_size, mat.slice_lengths, mat.slice_sets,
+                               mat.col_idxs, mat.values, row_perm=mat.row_perm)
+        whole._pieces = None
+        whole.apply(vec(dev, bv), x_whole)
+        plan = mat._pieces[0].cpu().numpy()
+        nblk = -(-mat.num_slices // (128 // mat.slice_size))
+        one = np.nonzero(np.diff(plan[:nblk + 1]) == 1)[0]
+        rows = (one[:, None] * 128 + np.arange(128)[None, :]).ravel()
+        rows = rows[rows < n]
+        if mat.row_perm is not None:
+            rows = mat.row_perm.cpu().numpy()[rows]
+        np.testing.assert_array_equal(host(x)[rows], host(x_whole)[rows])
+    # a solver through the split operator (row-splitting: epilogue pass), SPD matrix with
+    # the same long rows: CG on split SELL-P against CG on CSR
+    if vdt == np.float64:
+        import scipy.sparse as sps
+        B = sps.csr_matrix((np.abs(v).astype(np.float64), ci, rp), shape=(n, n))
+        S_ = (B + B.T).tocsr()
+        S_ = (S_ + sps.diags(np.asarray(abs(S_).sum(axis=1)).ravel() + 1.0)).tocsr()
+        S_.sort_indices()
+        spd = csr(dev, S_.indptr.astype(np.int32), S_.indices.astype(np.int32), S_.data)
+        sell = sp.sellp_from_csr(spd, 64)
+        assert sell._pieces is not None
+        crit = [sp.Iteration(500), sp.ResidualNorm(1e-10)]
+        logs = []
+        for mat in (spd, sell):
+            x = vec(dev, np.zeros(n))
+            logs.append((sp.Cg(mat, criteria=crit, preconditioner=sp.jacobi_create(spd)).solve(vec(dev, bv), x),
+                         host(x)))
+        (l0, x0), (l1, x1) = logs
+        assert l0.converged and l1.converged and abs(l0.iterations - l1.iterations) <= 1
+        np.testing.assert_allclose(x1, x0, rtol=1e-8, atol=1e-10)
