@@ -89,6 +89,7 @@ struct CgPArgs {
     int pf;  // update-phase L2 prefetch distance in blocks (SPARSEB200_CG_PF; 0 = off; 128^3:
              // 1 / 2 / 3 blocks ahead 72.4 / 73.2 / 74.4 us per iteration)
     void *q1;  // single-sync kernel: second q buffer (z doubles as the second r buffer)
+    int xa;    // two-barrier kernel: x update deferred into the next SpMV phase
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -235,6 +236,11 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
     double rz = c->rz, beta = 0.0;
     const double bnorm = c->bnorm;
     bool first = true;
+    // x update deferred into the next SpMV phase (x_{k-1} += alpha_{k-1} p_{k-1} where the
+    // own p_{k-1} is already loaded): the update phase no longer reads p or x
+    const bool xa = a.xa;
+    bool flush = false;
+    double alpha = 0.0;
     V *pold = (V *)a.p0, *pnew = (V *)a.p1;
     unsigned long long tp[4] = {0, 0, 0, 0}, t0 = gtimer(), t1;
     for (;;) {
@@ -269,7 +275,9 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
                         if (k + j < ke) acc = addd(acc, mulp(vv[j], bb[j]));
                 }
                 const V qi = (V)acc;
-                const V pi = cg_direction(first, beta, z[i], pold[i]);
+                const V po = pold[i];
+                const V pi = cg_direction(first, beta, z[i], po);
+                if (xa && !first) x[i] = axpy_e(alpha, po, x[i]);  // x_{k-1} (deferred update)
                 q[i] = qi;
                 pnew[i] = pi;
                 part[0] = addd(part[0], mulp(pi, qi));
@@ -289,7 +297,7 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
             if (bid == 0 && tid == 0) breakdown(c, it);
             break;
         }
-        const double alpha = rz / pq[0];
+        alpha = rz / pq[0];
         // ---- B: x += alpha p_k; r -= alpha q; z = M r; r.r, r.z on the rows of this CTA's
         // own SpMV blocks (same moving window over memory as phase A; measured faster than
         // a balanced contiguous split, which scatters the accesses over the whole vectors)
@@ -306,12 +314,12 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
             if (a.pf && tid < 5 && j + a.pf < kb) {
                 const int64_t nb = blk + (int64_t)a.pf * G;
                 const int64_t b0 = cg_block_row(nb, bq, rem), b1 = min(cg_block_row(nb + 1, bq, rem), n);
-                const V *vp = tid == 0 ? x : tid == 1 ? r : tid == 2 ? q : tid == 3 ? pnew : inv;
+                const V *vp = tid == 0 ? (xa ? nullptr : x) : tid == 1 ? r : tid == 2 ? q : tid == 3 ? (xa ? nullptr : pnew) : inv;
                 if (vp) l2_prefetch_range(vp + b0, vp + b1);
             }
             if (own) {
-                const V pi = pnew[i], qi = q[i];
-                x[i] = axpy_e(alpha, pi, x[i]);
+                const V qi = q[i];
+                if (!xa) x[i] = axpy_e(alpha, pnew[i], x[i]);
                 const V ri = axpy_e(-alpha, qi, r[i]);
                 const V zi = inv ? vmul(ri, inv[i]) : ri;
                 r[i] = ri;
@@ -337,10 +345,12 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
         }
         if (reason != STOP_NONE) {
             if (bid == 0 && tid == 0) finish_with(c, it, reason);
+            flush = xa;
             break;
         }
         if (!isfinite(tot[1]) || rz == 0.0) {
             if (bid == 0 && tid == 0) breakdown(c, it);
+            flush = xa;
             break;
         }
         beta = tot[1] / rz;
@@ -350,6 +360,12 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
         pold = pnew;
         pnew = t;
     }
+    if (flush)  // the last iteration's x update (x_k = x_{k-1} + alpha_k p_k, own rows)
+        for (int j = 0; j < kb; ++j) {
+            const int64_t blk = bid + (int64_t)j * G;
+            const int64_t i = cg_block_row(blk, bq, rem) + tid;
+            if (i < min(cg_block_row(blk + 1, bq, rem), n)) x[i] = axpy_e(alpha, pnew[i], x[i]);
+        }
     if (tid == 0 && bid < nblk) mbar_wait(&bar[seq & 1], (seq >> 1) & 1);  // drain the prefetch
     if (a.prof && tid == 0) {  // SM of every CTA (profiling: arrival spread by SM / die)
         unsigned smid;
@@ -932,6 +948,8 @@ sb_status cg_solve(const SolveArgs &a) {
         static const int pf = getenv("SPARSEB200_CG_PF") ? atoi(getenv("SPARSEB200_CG_PF")) : 1;
         pa.pf = pf;
         pa.q1 = g_cg_sync.load() == 1 ? q1 : nullptr;  // single-sync kernel (opt-in)
+        static const int xa = getenv("SPARSEB200_CG_XA") ? atoi(getenv("SPARSEB200_CG_XA")) : 0;  // 128^3: 75.8 vs 73.1 us, off
+        pa.xa = xa;
         cudaError_t le;
         if (cg_persistent_launch<V, I>(M, pa, a.st, le)) {
             g_cg_last_loop = 3;
