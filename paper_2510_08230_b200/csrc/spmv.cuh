@@ -234,6 +234,7 @@ __global__ void __launch_bounds__(R, epi_min_ctas<Epi>(R)) csr_stream_kernel(int
         return;
     }
     epi_prepare(epi);
+    const bool unit = ldb == 1;
     epi_part_t<Epi> part[Epi::N] = {};
     for (int it = 0; blk < nblk; blk += gridDim.x, ++it) {
         const int s = it % NS;
@@ -251,35 +252,48 @@ __global__ void __launch_bounds__(R, epi_min_ctas<Epi>(R)) csr_stream_kernel(int
         const StreamMeta m = meta[s];
         const int64_t i = m.r0 + tid;
         if (i < m.r1) {
+            // 32-bit stage offsets of the row (the stage holds < 2^31 entries); the column
+            // gathers of a unit-stride b are one wide multiply-add each (the strided form
+            // is a separate instantiation, so the loop carries no 64-bit multiply)
             const int64_t kb = sr[i - m.ar], ke = sr[i + 1 - m.ar];
-            double acc = 0.0;
-            int64_t k = kb;
-            for (; k + 8 <= ke; k += 8) {
-                V vv[8], bb[8];
+            const int ov = (int)(kb - m.av), oc = (int)(kb - m.ac), cnt = (int)(ke - kb);
+            auto rowsum = [&](auto unit_tag) -> double {
+                constexpr bool U1 = decltype(unit_tag)::value;
+                auto off = [&](int64_t c) -> int64_t {
+                    if constexpr (U1) return c;
+                    else return c * ldb;
+                };
+                double acc = 0.0;
+                int t = 0;
+                for (; t + 8 <= cnt; t += 8) {
+                    V vv[8], bb[8];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    vv[j] = sv[k + j - m.av];
-                    bb[j] = gather_b(epi, b, (int64_t)sc[k + j - m.ac] * ldb);
+                    for (int j = 0; j < 8; ++j) {
+                        vv[j] = sv[ov + t + j];
+                        bb[j] = gather_b(epi, b, off((int64_t)sc[oc + t + j]));
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc = addd(acc, mulp(vv[j], bb[j]));
                 }
+                if (t < cnt) {
+                    // branch-free tail: lanes past the row end re-read its last entry (an
+                    // L1 hit) and are masked at the ordered adds, so every gather of the row
+                    // is in flight before the first add (a gather hook that computes on the
+                    // loaded values would otherwise serialise one latency per entry)
+                    V vv[8], bb[8];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc = addd(acc, mulp(vv[j], bb[j]));
-            }
-            if (k < ke) {
-                // branch-free tail: lanes past the row end re-read its last entry (an L1
-                // hit) and are masked at the ordered adds, so every gather of the row is
-                // in flight before the first add (a gather hook that computes on the
-                // loaded values would otherwise serialise one latency per entry)
-                V vv[8], bb[8];
+                    for (int j = 0; j < 8; ++j) {
+                        const int kk = t + j < cnt ? t + j : cnt - 1;
+                        vv[j] = sv[ov + kk];
+                        bb[j] = gather_b(epi, b, off((int64_t)sc[oc + kk]));
+                    }
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const int64_t kk = k + j < ke ? k + j : ke - 1;
-                    vv[j] = sv[kk - m.av];
-                    bb[j] = gather_b(epi, b, (int64_t)sc[kk - m.ac] * ldb);
+                    for (int j = 0; j < 8; ++j)
+                        if (t + j < cnt) acc = addd(acc, mulp(vv[j], bb[j]));
                 }
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    if (k + j < ke) acc = addd(acc, mulp(vv[j], bb[j]));
-            }
+                return acc;
+            };
+            const double acc = unit ? rowsum(std::true_type{}) : rowsum(std::false_type{});
             epi.row(i, acc, part);
         }
         __syncthreads();  // stage s fully consumed before it is re-issued
