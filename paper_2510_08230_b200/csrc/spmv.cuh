@@ -75,6 +75,13 @@ __device__ __forceinline__ V gather_b(const Epi &e, const V *__restrict__ b, int
     if constexpr (epi_has_gather<Epi>::value) return e.gather(off);
     else return __ldg(b + off);
 }
+// column offset into b: unit stride (the common single-vector case) as its own
+// instantiation, so the gather is one wide multiply-add instead of a 64-bit multiply
+template <bool U1>
+__device__ __forceinline__ int64_t bidx(int64_t c, int64_t ldb) {
+    if constexpr (U1) return c;
+    else return c * ldb;
+}
 template <class Epi>
 __device__ __forceinline__ void epi_prepare(Epi &e) {
     if constexpr (epi_has_prepare<Epi>::value) e.prepare();
@@ -660,7 +667,7 @@ struct TileJob {
 
 // fp32 direct tiles are capped to 32 registers for 8 CTAs per SM (350 -> 333 us on config
 // #3); the same cap makes fp64 slower (381 -> 745 us), which keeps the compiler's choice
-template <class V, class I, int NT, int C, int RCAP, bool DIRECT = false, int PF = 0>
+template <class V, class I, int NT, int C, int RCAP, bool DIRECT = false, int PF = 0, bool U1 = false>
 __global__ void __launch_bounds__(NT, (DIRECT && sizeof(V) == 4) ? 2048 / NT : 0) csr_tile_kernel(int64_t rows, int64_t nnz, const I *__restrict__ rp,
                                                        const I *__restrict__ ci, const V *__restrict__ val,
                                                        const V *__restrict__ b, int64_t ldb, V *x, int64_t ldx,
@@ -752,7 +759,7 @@ __global__ void __launch_bounds__(NT, (DIRECT && sizeof(V) == 4) ? 2048 / NT : 0
                 vv[u] = ld_stream(val + k0 + jj);
             }
 #pragma unroll
-            for (int u = 0; u < PER; ++u) bb[u] = __ldg(b + (int64_t)cc[u] * ldb);
+            for (int u = 0; u < PER; ++u) bb[u] = __ldg(b + bidx<U1>((int64_t)cc[u], ldb));
 #pragma unroll
             for (int u = 0; u < PER; ++u) {
                 const int j = tid + u * NT;
@@ -763,7 +770,7 @@ __global__ void __launch_bounds__(NT, (DIRECT && sizeof(V) == 4) ? 2048 / NT : 0
 #pragma unroll
             for (int u = 0; u < PER; ++u) {
                 const int j = tid + u * NT;
-                bb[u] = __ldg(b + (int64_t)sc[j < cnt ? j : cnt - 1] * ldb);
+                bb[u] = __ldg(b + bidx<U1>((int64_t)sc[j < cnt ? j : cnt - 1], ldb));
             }
 #pragma unroll
             for (int u = 0; u < PER; ++u) {
@@ -1084,7 +1091,7 @@ __device__ __forceinline__ void load_column(const V *__restrict__ val, const I *
 // Accumulate `len` padded columns (column k at base0 + k*kstride) for RPT rows, four
 // columns per step with all loads and gathers issued before the ordered adds (padding
 // col = -1 is skipped, so each row's sum keeps the CSR order exactly).
-template <class V, class I, int RPT, class Epi>
+template <class V, class I, int RPT, class Epi, bool U1>
 __device__ __forceinline__ void padded_rows(const Epi &epi, const V *__restrict__ val, const I *__restrict__ col,
                                             const V *__restrict__ b, int64_t ldb, int64_t base0,
                                             int64_t kstride, int64_t len, double (&acc)[RPT]) {
@@ -1099,9 +1106,9 @@ __device__ __forceinline__ void padded_rows(const Epi &epi, const V *__restrict_
 #pragma unroll
             for (int r = 0; r < RPT; ++r) {
                 if constexpr (epi_has_gather<Epi>::value)  // branch-free: padding gathers col 0
-                    gg[u][r] = gather_b(epi, b, (int64_t)(cc[u][r] >= 0 ? cc[u][r] : 0) * ldb);
+                    gg[u][r] = gather_b(epi, b, bidx<U1>((int64_t)(cc[u][r] >= 0 ? cc[u][r] : 0), ldb));
                 else  // predicated plain loads: heavily padded slices issue no pad gathers
-                    gg[u][r] = cc[u][r] >= 0 ? __ldg(b + (int64_t)cc[u][r] * ldb) : (V)0;
+                    gg[u][r] = cc[u][r] >= 0 ? __ldg(b + bidx<U1>((int64_t)cc[u][r], ldb)) : (V)0;
             }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -1115,14 +1122,14 @@ __device__ __forceinline__ void padded_rows(const Epi &epi, const V *__restrict_
         load_column<V, I, RPT>(val, col, base0 + k * kstride, vv, cc);
 #pragma unroll
         for (int r = 0; r < RPT; ++r)
-            if (cc[r] >= 0) acc[r] = addd(acc[r], mulp(vv[r], gather_b(epi, b, (int64_t)cc[r] * ldb)));
+            if (cc[r] >= 0) acc[r] = addd(acc[r], mulp(vv[r], gather_b(epi, b, bidx<U1>((int64_t)cc[r], ldb))));
     }
 }
 
 // ============================================================ ELL (column-major)
 // RPT consecutive rows per thread with 16-byte vector loads of values (and 8/16-byte
 // loads of column indices); per-row order is the stored order -> bitwise = reference.
-template <class V, class I, int RPT, class Epi>
+template <class V, class I, int RPT, class Epi, bool U1>
 __global__ void __launch_bounds__(256) ell_kernel(int64_t rows, int64_t width, int64_t stride,
                                                   const I *__restrict__ col, const V *__restrict__ val,
                                                   const V *__restrict__ b, int64_t ldb, Epi epi) {
@@ -1136,7 +1143,7 @@ __global__ void __launch_bounds__(256) ell_kernel(int64_t rows, int64_t width, i
         double acc[RPT];
 #pragma unroll
         for (int r = 0; r < RPT; ++r) acc[r] = 0.0;
-        padded_rows<V, I, RPT>(epi, val, col, b, ldb, i0, stride, width, acc);
+        padded_rows<V, I, RPT, Epi, U1>(epi, val, col, b, ldb, i0, stride, width, acc);
 #pragma unroll
         for (int r = 0; r < RPT; ++r)
             if (i0 + r < rows) epi.row(i0 + r, acc[r], part);
@@ -1147,7 +1154,7 @@ __global__ void __launch_bounds__(256) ell_kernel(int64_t rows, int64_t width, i
 // ============================================================ SELL-P
 // Slices of S rows; entry k of row i (slice s) at (slice_sets[s] + k)*S + i%S.
 // RPT consecutive rows of one slice per thread (S % RPT == 0), vector loads.
-template <class V, class I, int RPT, class Epi>
+template <class V, class I, int RPT, class Epi, bool U1>
 __global__ void __launch_bounds__(256) sellp_kernel(int64_t rows, int64_t S,
                                                     const I *__restrict__ slice_lengths,
                                                     const I *__restrict__ slice_sets,
@@ -1169,7 +1176,7 @@ __global__ void __launch_bounds__(256) sellp_kernel(int64_t rows, int64_t S,
         double acc[RPT];
 #pragma unroll
         for (int r = 0; r < RPT; ++r) acc[r] = 0.0;
-        padded_rows<V, I, RPT>(epi, val, col, b, ldb, off, S, len, acc);
+        padded_rows<V, I, RPT, Epi, U1>(epi, val, col, b, ldb, off, S, len, acc);
 #pragma unroll
         for (int r = 0; r < RPT; ++r)
             if (i0 + r < rows) epi.row(perm ? (int64_t)perm[i0 + r] : i0 + r, acc[r], part);
@@ -1190,7 +1197,7 @@ struct SellpBlockMeta {
     int32_t len[4], off[4];  // per slice: length, first entry relative to the block start
 };
 
-template <class V, class I, int S, class Epi>
+template <class V, class I, int S, class Epi, bool U1>
 __global__ void __launch_bounds__(128) sellp_block_kernel(int64_t rows, int64_t nslices,
                                                            const I *__restrict__ sl,
                                                            const I *__restrict__ ss,
@@ -1272,9 +1279,9 @@ __global__ void __launch_bounds__(128) sellp_block_kernel(int64_t rows, int64_t 
                     vv[u] = sv[dv + e];
                     cc[u] = sc[dc + e];
                     if constexpr (epi_has_gather<Epi>::value)  // padding: col 0, masked below
-                        bb[u] = gather_b(epi, b, (int64_t)(cc[u] >= 0 ? cc[u] : 0) * ldb);
+                        bb[u] = gather_b(epi, b, bidx<U1>((int64_t)(cc[u] >= 0 ? cc[u] : 0), ldb));
                     else
-                        bb[u] = cc[u] >= 0 ? __ldg(b + (int64_t)cc[u] * ldb) : (V)0;
+                        bb[u] = cc[u] >= 0 ? __ldg(b + bidx<U1>((int64_t)cc[u], ldb)) : (V)0;
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
@@ -1288,7 +1295,7 @@ __global__ void __launch_bounds__(128) sellp_block_kernel(int64_t rows, int64_t 
                     const int64_t e = o + (int64_t)(k + u < len ? k + u : len - 1) * S;
                     vv[u] = sv[dv + e];
                     cc[u] = k + u < len ? sc[dc + e] : (I)-1;
-                    bb[u] = gather_b(epi, b, (int64_t)(cc[u] >= 0 ? cc[u] : 0) * ldb);
+                    bb[u] = gather_b(epi, b, bidx<U1>((int64_t)(cc[u] >= 0 ? cc[u] : 0), ldb));
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
@@ -1321,7 +1328,7 @@ struct SellpMeta {
     int32_t last;            // last chunk of the block: emit the rows
 };
 
-template <class V, class I, int S, class Epi>
+template <class V, class I, int S, class Epi, bool U1>
 __global__ void __launch_bounds__(128) sellp_chunk_kernel(int64_t rows, int64_t nslices,
                                                            const I *__restrict__ sl,
                                                            const I *__restrict__ ss,
@@ -1424,9 +1431,9 @@ __global__ void __launch_bounds__(128) sellp_chunk_kernel(int64_t rows, int64_t 
                     vv[u] = sv[ov + (int64_t)kk * S];
                     cc[u] = k + u < kend ? sc[oc + (int64_t)kk * S] : (I)-1;
                     if constexpr (epi_has_gather<Epi>::value)  // padding: col 0, masked below
-                        bb[u] = gather_b(epi, b, (int64_t)(cc[u] >= 0 ? cc[u] : 0) * ldb);
+                        bb[u] = gather_b(epi, b, bidx<U1>((int64_t)(cc[u] >= 0 ? cc[u] : 0), ldb));
                     else
-                        bb[u] = cc[u] >= 0 ? __ldg(b + (int64_t)cc[u] * ldb) : (V)0;
+                        bb[u] = cc[u] >= 0 ? __ldg(b + bidx<U1>((int64_t)cc[u], ldb)) : (V)0;
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
@@ -1453,7 +1460,7 @@ __global__ void __launch_bounds__(128) sellp_chunk_kernel(int64_t rows, int64_t 
 // sellp_piece_fixup_kernel adds them in piece order.  Plan (int64, built by the
 // frontend): pstart[nblk + 1] (first piece of each block), pblock[npieces] (block of each
 // piece), split[nsplit] (blocks of more than one piece).
-template <class V, class I, int S>
+template <class V, class I, int S, bool U1>
 __global__ void __launch_bounds__(128) sellp_piece_kernel(int64_t rows, int64_t nslices,
                                                            const I *__restrict__ sl,
                                                            const I *__restrict__ ss,
@@ -1555,7 +1562,7 @@ __global__ void __launch_bounds__(128) sellp_piece_kernel(int64_t rows, int64_t 
                     const int kk = k + u < kend ? k + u : kend - 1;
                     vv[u] = sv[ov + (int64_t)kk * S];
                     cc[u] = k + u < kend ? sc[oc + (int64_t)kk * S] : (I)-1;
-                    bb[u] = cc[u] >= 0 ? __ldg(b + (int64_t)cc[u] * ldb) : (V)0;
+                    bb[u] = cc[u] >= 0 ? __ldg(b + bidx<U1>((int64_t)cc[u], ldb)) : (V)0;
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u)

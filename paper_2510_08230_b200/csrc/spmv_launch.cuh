@@ -160,7 +160,10 @@ cudaError_t launch_csr_tile_t(const sb_csr &A, const V *b, int64_t ldb, V *x, in
     const sb_csr_plan &P = *A.plan;
     const int64_t ntiles = P.num_tiles / 2;
     constexpr size_t smem = TileLayout<V, I, C, RCAP, DIRECT>::SMEM;
-    auto kern = csr_tile_kernel<V, I, NT, C, RCAP, DIRECT, PF>;
+    // unit-stride gathers: fp64 369 us either way on config #3, fp32 333 -> 358 us (the
+    // 32-register fp32 kernel schedules worse), so fp64 only
+    auto kern = ldb == 1 && sizeof(V) == 8 ? csr_tile_kernel<V, I, NT, C, RCAP, DIRECT, PF, true>
+                                           : csr_tile_kernel<V, I, NT, C, RCAP, DIRECT, PF, false>;
     ensure_max_smem((const void *)kern);
     int grid = persistent_grid(kern, NT, smem);
     if (grid > ntiles) grid = (int)ntiles;
@@ -317,14 +320,14 @@ cudaError_t ell_apply(const sb_ell &A, const V *b, int64_t ldb, const Epi &epi, 
     const bool vec_ok = (A.stride % RPT == 0) && ((uintptr_t)A.values % 16 == 0) &&
                         ((uintptr_t)A.col_idxs % (RPT * sizeof(I) >= 16 ? 16 : RPT * sizeof(I)) == 0);
     if (vec_ok) {
-        auto kern = ell_kernel<V, I, RPT, Epi>;
+        auto kern = ldb == 1 ? ell_kernel<V, I, RPT, Epi, true> : ell_kernel<V, I, RPT, Epi, false>;
         int grid = persistent_grid(kern, 256, 0);
         const int64_t need = ceil_div(ceil_div(A.rows, RPT), 256);
         if (grid > need) grid = (int)need;
         kern<<<grid, 256, 0, st>>>(A.rows, A.width, A.stride, (const I *)A.col_idxs,
                                    (const V *)A.values, b, ldb, epi);
     } else {
-        auto kern = ell_kernel<V, I, 1, Epi>;
+        auto kern = ldb == 1 ? ell_kernel<V, I, 1, Epi, true> : ell_kernel<V, I, 1, Epi, false>;
         int grid = persistent_grid(kern, 256, 0);
         const int64_t need = ceil_div(A.rows, 256);
         if (grid > need) grid = (int)need;
@@ -345,9 +348,10 @@ cudaError_t launch_sellp_stream(const sb_sellp &A, const V *b, int64_t ldb, cons
     const size_t off_c = (cap_v * sizeof(V) + 15) & ~size_t(15);
     const size_t stage = (off_c + cap_c * sizeof(I) + 15) & ~size_t(15);
     // whole slice blocks when the largest fits a 2048-entry stage, else column chunks
-    auto kern = A.max_block_entries <= cap ? sellp_block_kernel<V, I, S, Epi> : sellp_chunk_kernel<V, I, S, Epi>;
-    ensure_max_smem((const void *)sellp_block_kernel<V, I, S, Epi>);
-    ensure_max_smem((const void *)sellp_chunk_kernel<V, I, S, Epi>);
+    auto kern = A.max_block_entries <= cap
+                    ? (ldb == 1 ? sellp_block_kernel<V, I, S, Epi, true> : sellp_block_kernel<V, I, S, Epi, false>)
+                    : (ldb == 1 ? sellp_chunk_kernel<V, I, S, Epi, true> : sellp_chunk_kernel<V, I, S, Epi, false>);
+    ensure_max_smem((const void *)kern);
     int grid = persistent_grid(kern, 128, 2 * stage);
     const int64_t nblk = ceil_div(A.num_slices, 128 / S);
     if (grid > nblk) grid = (int)nblk;
@@ -366,7 +370,7 @@ cudaError_t launch_sellp_pieces(const sb_sellp &A, const V *b, int64_t ldb, V *x
     const size_t off_c = (cap_v * sizeof(V) + 15) & ~size_t(15);
     const size_t stage = (off_c + cap_c * sizeof(I) + 15) & ~size_t(15);
     if (A.piece_entries <= 0 || A.piece_entries % (cap / S * S) != 0) return cudaErrorInvalidValue;
-    auto kern = sellp_piece_kernel<V, I, S>;
+    auto kern = ldb == 1 ? sellp_piece_kernel<V, I, S, true> : sellp_piece_kernel<V, I, S, false>;
     ensure_max_smem((const void *)kern);
     int grid = persistent_grid(kern, 128, 2 * stage);
     if (grid > A.num_pieces) grid = (int)A.num_pieces;
@@ -414,7 +418,7 @@ cudaError_t sellp_apply(const sb_sellp &A, const V *b, int64_t ldb, V *x_out, in
                         ((uintptr_t)A.col_idxs % (RPT * sizeof(I) >= 16 ? 16 : RPT * sizeof(I)) == 0);
     const int64_t slots = A.num_slices * A.slice_size;
     if (vec_ok) {
-        auto kern = sellp_kernel<V, I, RPT, Epi>;
+        auto kern = ldb == 1 ? sellp_kernel<V, I, RPT, Epi, true> : sellp_kernel<V, I, RPT, Epi, false>;
         int grid = persistent_grid(kern, 256, 0);
         const int64_t need = ceil_div(slots / RPT, 256);
         if (grid > need) grid = (int)(need > 0 ? need : 1);
@@ -422,7 +426,7 @@ cudaError_t sellp_apply(const sb_sellp &A, const V *b, int64_t ldb, V *x_out, in
                                    (const I *)A.slice_sets, (const I *)A.col_idxs,
                                    (const V *)A.values, b, ldb, epi, (const I *)A.row_perm);
     } else {
-        auto kern = sellp_kernel<V, I, 1, Epi>;
+        auto kern = ldb == 1 ? sellp_kernel<V, I, 1, Epi, true> : sellp_kernel<V, I, 1, Epi, false>;
         int grid = persistent_grid(kern, 256, 0);
         const int64_t need = ceil_div(slots, 256);
         if (grid > need) grid = (int)(need > 0 ? need : 1);
