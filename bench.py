@@ -234,13 +234,15 @@ def _spmv_roofline(a, dev, stream, torch, sp):
     peak, peak_kind = _peaks()
     achieved = spmv_bytes / (spmv_ms / 1e3) / 1e9
     traffic = None
-    try:  # DRAM bytes per launch from the committed ncu --set full capture of this kernel
-        with open(os.path.join(REPO, "profiles", "r1_spmv_traffic.json")) as fh:
-            t = json.load(fh)
-        if t["algorithmic_bytes"] == spmv_bytes:
-            traffic = t["traffic"]
-    except Exception:
-        pass
+    for name in ("r2_spmv_traffic.json", "r1_spmv_traffic.json"):  # newest committed capture first
+        try:  # DRAM bytes per launch from the committed ncu --set full capture of this kernel
+            with open(os.path.join(REPO, "profiles", name)) as fh:
+                t = json.load(fh)
+            if t["algorithmic_bytes"] == spmv_bytes:
+                traffic = t["traffic"]
+                break
+        except Exception:
+            pass
     return spmv_ms, spmv_bytes, {
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
         "traffic": traffic, "kernel": f"csr_{a.kernel}_kernel<double,int>",
@@ -250,13 +252,14 @@ def _spmv_roofline(a, dev, stream, torch, sp):
 def _persistent_traffic(iter_bytes):
     """DRAM bytes per CG iteration of the persistent kernel from the committed ncu
     --set full capture (profiles/), if it was taken for this byte model."""
-    try:
-        with open(os.path.join(REPO, "profiles", "r1_cg_persistent_traffic.json")) as fh:
-            t = json.load(fh)
-        if t["algorithmic_bytes_per_iteration"] == iter_bytes:
-            return t["traffic_per_iteration"]
-    except Exception:
-        pass
+    for name in ("r2_cg_persistent_traffic.json", "r1_cg_persistent_traffic.json"):
+        try:
+            with open(os.path.join(REPO, "profiles", name)) as fh:
+                t = json.load(fh)
+            if t["algorithmic_bytes_per_iteration"] == iter_bytes:
+                return t["traffic_per_iteration"]
+        except Exception:
+            pass
     return None
 
 
