@@ -1265,9 +1265,9 @@ __global__ void __launch_bounds__(128) sellp_block_kernel(int64_t rows, int64_t 
         const int j = tid / S, l = tid % S;
         const int64_t i = (m.s0 + j) * S + l;
         if (j < SPB && i < rows) {
-            const int64_t dv = m.dv, dc = m.dc;
+            // 32-bit stage offsets (a stage holds < 2^31 entries)
             const int len = m.len[j];
-            const int64_t o = m.off[j] + l;
+            const int ov = (int)(m.dv + m.off[j] + l), oc = (int)(m.dc + m.off[j] + l);
             double acc = 0.0;
             int k = 0;
             for (; k + 8 <= len; k += 8) {
@@ -1275,9 +1275,8 @@ __global__ void __launch_bounds__(128) sellp_block_kernel(int64_t rows, int64_t 
                 I cc[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    const int64_t e = o + (int64_t)(k + u) * S;
-                    vv[u] = sv[dv + e];
-                    cc[u] = sc[dc + e];
+                    vv[u] = sv[ov + (k + u) * S];
+                    cc[u] = sc[oc + (k + u) * S];
                     if constexpr (epi_has_gather<Epi>::value)  // padding: col 0, masked below
                         bb[u] = gather_b(epi, b, bidx<U1>((int64_t)(cc[u] >= 0 ? cc[u] : 0), ldb));
                     else
@@ -1292,9 +1291,9 @@ __global__ void __launch_bounds__(128) sellp_block_kernel(int64_t rows, int64_t 
                 I cc[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {  // branch-free tail (see csr_stream_kernel)
-                    const int64_t e = o + (int64_t)(k + u < len ? k + u : len - 1) * S;
-                    vv[u] = sv[dv + e];
-                    cc[u] = k + u < len ? sc[dc + e] : (I)-1;
+                    const int e = (k + u < len ? k + u : len - 1) * S;
+                    vv[u] = sv[ov + e];
+                    cc[u] = k + u < len ? sc[oc + e] : (I)-1;
                     bb[u] = gather_b(epi, b, bidx<U1>((int64_t)(cc[u] >= 0 ? cc[u] : 0), ldb));
                 }
 #pragma unroll
