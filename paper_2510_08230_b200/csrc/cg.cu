@@ -173,7 +173,9 @@ __host__ __device__ __forceinline__ int64_t cg_block_row(int64_t b, int64_t bq, 
     return 32 * (b * bq + (b < rem ? b : rem));
 }
 
-template <class V, class I, int R>
+// PROF: phase timers and barrier arrival stamps (SPARSEB200_CG_PROFILE; a separate
+// instantiation, so the timed kernel carries no timer registers)
+template <class V, class I, int R, bool PROF = false>
 __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar[2];
@@ -242,7 +244,7 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
     bool flush = false;
     double alpha = 0.0;
     V *pold = (V *)a.p0, *pnew = (V *)a.p1;
-    unsigned long long tp[4] = {0, 0, 0, 0}, t0 = gtimer(), t1;
+    unsigned long long tp[4] = {0, 0, 0, 0}, t0 = PROF ? gtimer() : 0, t1;
     for (;;) {
         // ---- A: q = A p_k, p_k = z + beta p_{k-1} gathered on the fly
         double part[1] = {0.0};
@@ -259,20 +261,22 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
             const StreamMeta m = meta[s];
             const int64_t i = m.r0 + tid;
             if (i < m.r1) {
+                // 32-bit stage offsets of the row (as csr_stream_kernel)
                 const int64_t kb = sr[i - m.ar], ke = sr[i + 1 - m.ar];
+                const int ov = (int)(kb - m.av), oc = (int)(kb - m.ac), cnt = (int)(ke - kb);
                 double acc = 0.0;
-                for (int64_t k = kb; k < ke; k += 8) {
+                for (int t = 0; t < cnt; t += 8) {
                     V vv[8], bb[8];
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        const int64_t kk = k + j < ke ? k + j : ke - 1;
-                        const int64_t col = (int64_t)sc[kk - m.ac];
-                        vv[j] = sv[kk - m.av];
+                        const int kk = t + j < cnt ? t + j : cnt - 1;
+                        const int64_t col = (int64_t)sc[oc + kk];
+                        vv[j] = sv[ov + kk];
                         bb[j] = cg_direction(first, beta, z[col], pold[col]);
                     }
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
-                        if (k + j < ke) acc = addd(acc, mulp(vv[j], bb[j]));
+                        if (t + j < cnt) acc = addd(acc, mulp(vv[j], bb[j]));
                 }
                 const V qi = (V)acc;
                 const V po = pold[i];
@@ -284,14 +288,18 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
             }
             __syncthreads();  // stage s consumed before it is re-issued
         }
-        t1 = gtimer();
-        tp[0] += t1 - t0;
-        t0 = t1;
+        if constexpr (PROF) {
+            t1 = gtimer();
+            tp[0] += t1 - t0;
+            t0 = t1;
+        }
         double pq[1];
-        grid_allreduce<1, R>(part, a.partials, count, ++epoch * G, pq, a.prof);
-        t1 = gtimer();
-        tp[1] += t1 - t0;
-        t0 = t1;
+        grid_allreduce<1, R>(part, a.partials, count, ++epoch * G, pq, PROF ? a.prof : nullptr);
+        if constexpr (PROF) {
+            t1 = gtimer();
+            tp[1] += t1 - t0;
+            t0 = t1;
+        }
         ++it;
         if (!isfinite(pq[0]) || pq[0] <= kBreakdownRtol * fabs(rz)) {
             if (bid == 0 && tid == 0) breakdown(c, it);
@@ -328,14 +336,18 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
                 part2[1] = addd(part2[1], mulp(ri, zi));
             }
         }
-        t1 = gtimer();
-        tp[2] += t1 - t0;
-        t0 = t1;
+        if constexpr (PROF) {
+            t1 = gtimer();
+            tp[2] += t1 - t0;
+            t0 = t1;
+        }
         double tot[2];
-        grid_allreduce<2, R>(part2, a.partials + G, count, ++epoch * G, tot, a.prof);
-        t1 = gtimer();
-        tp[3] += t1 - t0;
-        t0 = t1;
+        grid_allreduce<2, R>(part2, a.partials + G, count, ++epoch * G, tot, PROF ? a.prof : nullptr);
+        if constexpr (PROF) {
+            t1 = gtimer();
+            tp[3] += t1 - t0;
+            t0 = t1;
+        }
         const double rnorm = sqrt(tot[0]);
         int reason = check_criteria(c, it, rnorm, bnorm);
         if (reason == STOP_NONE && rnorm == 0.0) reason = STOP_RESIDUAL;
@@ -367,7 +379,7 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
             if (i < min(cg_block_row(blk + 1, bq, rem), n)) x[i] = axpy_e(alpha, pnew[i], x[i]);
         }
     if (tid == 0 && bid < nblk) mbar_wait(&bar[seq & 1], (seq >> 1) & 1);  // drain the prefetch
-    if (a.prof && tid == 0) {  // SM of every CTA (profiling: arrival spread by SM / die)
+    if (PROF && a.prof && tid == 0) {  // SM of every CTA (profiling: arrival spread by SM / die)
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         a.prof[19 * (size_t)G + bid] = smid;
@@ -375,7 +387,8 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
     if (bid == 0 && tid == 0) {
         c->rz = rz;
         c->beta = beta;
-        for (int k = 0; k < 4; ++k) c->tphase[k] = tp[k];
+        if (PROF)
+            for (int k = 0; k < 4; ++k) c->tphase[k] = tp[k];
         c->tphase[4] = G;
     }
 }
@@ -663,7 +676,7 @@ bool cg_persistent_launch_r(const sb_matrix &M, const CgPArgs &proto, bool singl
     // single-sync kernel: CTAs per SM from SPARSEB200_CG1_MB (threads per SM = MB R)
     static const int mb_env = getenv("SPARSEB200_CG1_MB") ? atoi(getenv("SPARSEB200_CG1_MB")) : 0;
     const int mb = (mb_env == 3 || mb_env == 4 ? mb_env : 3) * 256 / R;  // 3: 80 registers, 3 stages of 68 KB
-    auto kern = !single ? cg_persistent_kernel<V, I, R>
+    auto kern = !single ? (proto.prof ? cg_persistent_kernel<V, I, R, true> : cg_persistent_kernel<V, I, R, false>)
                 : mb * R == 768 ? cg1_persistent_kernel<V, I, R, 768 / R> : cg1_persistent_kernel<V, I, R, 1024 / R>;
     ensure_max_smem((const void *)kern);
     const int sms = device_info().sms;
