@@ -175,10 +175,13 @@ __host__ __device__ __forceinline__ int64_t cg_block_row(int64_t b, int64_t bq, 
 
 // PROF: phase timers and barrier arrival stamps (SPARSEB200_CG_PROFILE; a separate
 // instantiation, so the timed kernel carries no timer registers)
-template <class V, class I, int R, bool PROF = false>
+// BT: update-phase operands (q, p_k, x, r, M) TMA-staged two blocks ahead into the stage
+// slot the SpMV ring leaves free during the update (see below)
+template <class V, class I, int R, bool PROF = false, bool BT = false>
 __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar[2];
+    __shared__ __align__(8) uint64_t barB[2];
     __shared__ StreamMeta meta[2];
     Ctl *c = a.ctl;
     if (c->done) return;  // setup found the exact solution
@@ -208,9 +211,34 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
+        mbar_init(&barB[0], 1);
+        mbar_init(&barB[1], 1);
         mbar_fence_init();
     }
     __syncthreads();
+    // update-phase staging: the SpMV ring's free slot (the other one holds the next SpMV's
+    // first block) split into two halves, each holding one block's five operand ranges
+    constexpr size_t kVecB = ((size_t)R * sizeof(V) + 15) & ~size_t(15);
+    const size_t hb = (sb / 2) & ~size_t(15);
+    uint32_t bseq = 0;  // update-phase blocks consumed in this launch (half-slot bseq & 1)
+    int bpend = 0;      // update-phase blocks issued but not consumed
+    auto issueB = [&](int j, unsigned char *slot, int h, const V *pk) {  // thread 0 only
+        unsigned char *dst = slot + h * hb;
+        const int64_t blk = bid + (int64_t)j * G;
+        const int64_t r0 = cg_block_row(blk, bq, rem), r1 = min(cg_block_row(blk + 1, bq, rem), n);
+        const V *src[5] = {q, pk, x, r, inv};
+        uint32_t by[5], tot = 0;
+        int64_t base = r0;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+            by[v] = src[v] ? stage_range(src[v], r0, r1, n, reinterpret_cast<V *>(dst + v * kVecB), base) : 0;
+            tot += by[v];
+        }
+        mbar_arrive_expect_tx(&barB[h], tot);
+#pragma unroll
+        for (int v = 0; v < 5; ++v)
+            if (by[v]) bulk_g2s(dst + v * kVecB, src[v] + base, by[v], &barB[h]);
+    };
     auto issue = [&](int64_t blk, int s) {  // thread 0 only (as csr_stream_kernel)
         unsigned char *st = smem + s * sb;
         V *sv = reinterpret_cast<V *>(st);
@@ -293,6 +321,18 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
             tp[0] += t1 - t0;
             t0 = t1;
         }
+        unsigned char *fslot = smem + ((seq & 1) ^ 1) * sb;  // free during the update phase
+        if constexpr (BT) {
+            // q and p_k were just stored by this CTA's threads: order those generic writes
+            // before the async-proxy (TMA) reads, then stage the first two update blocks so
+            // their loads overlap barrier 1
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            __syncthreads();
+            if (tid == 0) {
+                for (int j = 0; j < 2 && j < kb; ++j) issueB(j, fslot, (bseq + j) & 1, pnew);
+            }
+            bpend = kb < 2 ? kb : 2;
+        }
         double pq[1];
         grid_allreduce<1, R>(part, a.partials, count, ++epoch * G, pq, PROF ? a.prof : nullptr);
         if constexpr (PROF) {
@@ -303,6 +343,8 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
         ++it;
         if (!isfinite(pq[0]) || pq[0] <= kBreakdownRtol * fabs(rz)) {
             if (bid == 0 && tid == 0) breakdown(c, it);
+            if (BT && tid == 0)  // no bulk copy outlives the CTA
+                for (int j = 0; j < bpend; ++j) mbar_wait(&barB[(bseq + j) & 1], ((bseq + j) >> 1) & 1);
             break;
         }
         alpha = rz / pq[0];
@@ -310,6 +352,30 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
         // own SpMV blocks (same moving window over memory as phase A; measured faster than
         // a balanced contiguous split, which scatters the accesses over the whole vectors)
         double part2[2] = {0.0, 0.0};
+        if constexpr (BT) {
+            for (int j = 0; j < kb; ++j, ++bseq) {
+                const int h = bseq & 1;
+                mbar_wait(&barB[h], (bseq >> 1) & 1);
+                const unsigned char *src = fslot + h * hb;
+                const V *sq = reinterpret_cast<const V *>(src), *sp = reinterpret_cast<const V *>(src + kVecB),
+                        *sx = reinterpret_cast<const V *>(src + 2 * kVecB), *sr = reinterpret_cast<const V *>(src + 3 * kVecB),
+                        *sd = reinterpret_cast<const V *>(src + 4 * kVecB);
+                const int64_t blk = bid + (int64_t)j * G;
+                const int64_t i = cg_block_row(blk, bq, rem) + tid;  // block rows start 32-aligned: slot index tid
+                if (i < min(cg_block_row(blk + 1, bq, rem), n)) {
+                    x[i] = axpy_e(alpha, sp[tid], sx[tid]);
+                    const V ri = axpy_e(-alpha, sq[tid], sr[tid]);
+                    const V zi = inv ? vmul(ri, sd[tid]) : ri;
+                    r[i] = ri;
+                    z[i] = zi;
+                    part2[0] = addd(part2[0], mulp(ri, ri));
+                    part2[1] = addd(part2[1], mulp(ri, zi));
+                }
+                __syncthreads();  // half-slot consumed before it is re-issued
+                if (tid == 0 && j + 2 < kb) issueB(j + 2, fslot, h, pnew);
+            }
+            bpend = 0;
+        } else
         for (int j = 0; j < kb; ++j) {
             const int64_t blk = bid + (int64_t)j * G;
             const int64_t i = cg_block_row(blk, bq, rem) + tid;
@@ -676,9 +742,6 @@ bool cg_persistent_launch_r(const sb_matrix &M, const CgPArgs &proto, bool singl
     // single-sync kernel: CTAs per SM from SPARSEB200_CG1_MB (threads per SM = MB R)
     static const int mb_env = getenv("SPARSEB200_CG1_MB") ? atoi(getenv("SPARSEB200_CG1_MB")) : 0;
     const int mb = (mb_env == 3 || mb_env == 4 ? mb_env : 3) * 256 / R;  // 3: 80 registers, 3 stages of 68 KB
-    auto kern = !single ? (proto.prof ? cg_persistent_kernel<V, I, R, true> : cg_persistent_kernel<V, I, R, false>)
-                : mb * R == 768 ? cg1_persistent_kernel<V, I, R, 768 / R> : cg1_persistent_kernel<V, I, R, 1024 / R>;
-    ensure_max_smem((const void *)kern);
     const int sms = device_info().sms;
     const int per_sm = single ? mb : 1024 / R;
     int64_t grid = (int64_t)per_sm * sms;
@@ -702,6 +765,15 @@ bool cg_persistent_launch_r(const sb_matrix &M, const CgPArgs &proto, bool singl
     const size_t smem = single ? 2 * Cg1Layout<V, I>(R, cap > 0 ? cap : 64).stage_bytes() + 16 * kb
                                : 2 * StreamLayout<V, I>(R, cap > 0 ? cap : 64).stage_bytes() + 16 * kb;
     if (smem > 220 * 1024) return false;
+    // staged update phase when one block's five operand ranges fit half a stage
+    static const int bt_env = getenv("SPARSEB200_CG_BT") ? atoi(getenv("SPARSEB200_CG_BT")) : 1;
+    const size_t sb_cap = StreamLayout<V, I>(R, cap > 0 ? cap : 64).stage_bytes();
+    const bool bt = bt_env && !proto.xa && 5 * (((size_t)R * sizeof(V) + 15) & ~size_t(15)) <= ((sb_cap / 2) & ~size_t(15));
+    auto kern = !single ? (proto.prof ? cg_persistent_kernel<V, I, R, true>
+                           : bt       ? cg_persistent_kernel<V, I, R, false, true>
+                                      : cg_persistent_kernel<V, I, R, false>)
+                : mb * R == 768 ? cg1_persistent_kernel<V, I, R, 768 / R> : cg1_persistent_kernel<V, I, R, 1024 / R>;
+    ensure_max_smem((const void *)kern);
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, R, smem) != cudaSuccess || occ < per_sm) {
         cudaGetLastError();
