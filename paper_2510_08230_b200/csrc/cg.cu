@@ -181,7 +181,7 @@ template <class V, class I, int R, bool PROF = false, bool BT = false>
 __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar[2];
-    __shared__ __align__(8) uint64_t barB[2];
+    __shared__ __align__(8) uint64_t barB[4];
     __shared__ StreamMeta meta[2];
     Ctl *c = a.ctl;
     if (c->done) return;  // setup found the exact solution
@@ -211,19 +211,19 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
-        mbar_init(&barB[0], 1);
-        mbar_init(&barB[1], 1);
+        for (int h = 0; h < 4; ++h) mbar_init(&barB[h], 1);
         mbar_fence_init();
     }
     __syncthreads();
-    // update-phase staging: the SpMV ring's free slot (the other one holds the next SpMV's
-    // first block) split into two halves, each holding one block's five operand ranges
+    // update-phase staging: with BT the SpMV ring issues the next SpMV's first block only
+    // after the update phase, so both stage slots are free during it: four half-slots,
+    // each holding one block's five operand ranges (four blocks in flight per CTA)
     constexpr size_t kVecB = ((size_t)R * sizeof(V) + 15) & ~size_t(15);
     const size_t hb = (sb / 2) & ~size_t(15);
-    uint32_t bseq = 0;  // update-phase blocks consumed in this launch (half-slot bseq & 1)
+    uint32_t bseq = 0;  // update-phase blocks consumed in this launch (half-slot bseq & 3)
     int bpend = 0;      // update-phase blocks issued but not consumed
-    auto issueB = [&](int j, unsigned char *slot, int h, const V *pk) {  // thread 0 only
-        unsigned char *dst = slot + h * hb;
+    auto issueB = [&](int j, int h, const V *pk) {  // thread 0 only
+        unsigned char *dst = smem + (h >> 1) * sb + (h & 1) * hb;
         const int64_t blk = bid + (int64_t)j * G;
         const int64_t r0 = cg_block_row(blk, bq, rem), r1 = min(cg_block_row(blk + 1, bq, rem), n);
         const V *src[5] = {q, pk, x, r, inv};
@@ -260,6 +260,7 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
         if (br) bulk_g2s(sr, rp + m.ar, br, &bar[s], pol);
     };
     uint32_t seq = 0;  // ring position: stage seq & 1, parity (seq >> 1) & 1
+    bool apend = true;  // a next-SpMV block is staged when the loop ends
     if (tid == 0 && bid < nblk) issue(bid, 0);
 
     int64_t it = c->iter;
@@ -280,7 +281,7 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
             const int s = seq & 1;
             const int64_t nxt = blk + G < nblk ? blk + G : bid;  // wrap: next SpMV's first block
             // (every block has <= R rows: nblk >= ceil(n / R))
-            if (tid == 0) issue(nxt, s ^ 1);
+            if (tid == 0 && (!BT || blk + G < nblk)) issue(nxt, s ^ 1);  // BT: wrap after the update
             mbar_wait(&bar[s], (seq >> 1) & 1);
             const unsigned char *st = smem + s * sb;
             const V *sv = reinterpret_cast<const V *>(st);
@@ -321,7 +322,6 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
             tp[0] += t1 - t0;
             t0 = t1;
         }
-        unsigned char *fslot = smem + ((seq & 1) ^ 1) * sb;  // free during the update phase
         if constexpr (BT) {
             // q and p_k were just stored by this CTA's threads: order those generic writes
             // before the async-proxy (TMA) reads, then stage the first two update blocks so
@@ -329,9 +329,9 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
             asm volatile("fence.proxy.async.global;" ::: "memory");
             __syncthreads();
             if (tid == 0) {
-                for (int j = 0; j < 2 && j < kb; ++j) issueB(j, fslot, (bseq + j) & 1, pnew);
+                for (int j = 0; j < 4 && j < kb; ++j) issueB(j, (bseq + j) & 3, pnew);
             }
-            bpend = kb < 2 ? kb : 2;
+            bpend = kb < 4 ? kb : 4;
         }
         double pq[1];
         grid_allreduce<1, R>(part, a.partials, count, ++epoch * G, pq, PROF ? a.prof : nullptr);
@@ -344,7 +344,8 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
         if (!isfinite(pq[0]) || pq[0] <= kBreakdownRtol * fabs(rz)) {
             if (bid == 0 && tid == 0) breakdown(c, it);
             if (BT && tid == 0)  // no bulk copy outlives the CTA
-                for (int j = 0; j < bpend; ++j) mbar_wait(&barB[(bseq + j) & 1], ((bseq + j) >> 1) & 1);
+                for (int j = 0; j < bpend; ++j) mbar_wait(&barB[(bseq + j) & 3], ((bseq + j) >> 2) & 1);
+            apend = !BT;  // BT: the next SpMV's first block is not staged yet
             break;
         }
         alpha = rz / pq[0];
@@ -354,9 +355,9 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
         double part2[2] = {0.0, 0.0};
         if constexpr (BT) {
             for (int j = 0; j < kb; ++j, ++bseq) {
-                const int h = bseq & 1;
-                mbar_wait(&barB[h], (bseq >> 1) & 1);
-                const unsigned char *src = fslot + h * hb;
+                const int h = bseq & 3;
+                mbar_wait(&barB[h], (bseq >> 2) & 1);
+                const unsigned char *src = smem + (h >> 1) * sb + (h & 1) * hb;
                 const V *sq = reinterpret_cast<const V *>(src), *sp = reinterpret_cast<const V *>(src + kVecB),
                         *sx = reinterpret_cast<const V *>(src + 2 * kVecB), *sr = reinterpret_cast<const V *>(src + 3 * kVecB),
                         *sd = reinterpret_cast<const V *>(src + 4 * kVecB);
@@ -372,9 +373,10 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
                     part2[1] = addd(part2[1], mulp(ri, zi));
                 }
                 __syncthreads();  // half-slot consumed before it is re-issued
-                if (tid == 0 && j + 2 < kb) issueB(j + 2, fslot, h, pnew);
+                if (tid == 0 && j + 4 < kb) issueB(j + 4, h, pnew);
             }
             bpend = 0;
+            if (tid == 0 && bid < nblk) issue(bid, seq & 1);  // the next SpMV's first block (overlaps barrier 2)
         } else
         for (int j = 0; j < kb; ++j) {
             const int64_t blk = bid + (int64_t)j * G;
@@ -444,7 +446,7 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
             const int64_t i = cg_block_row(blk, bq, rem) + tid;
             if (i < min(cg_block_row(blk + 1, bq, rem), n)) x[i] = axpy_e(alpha, pnew[i], x[i]);
         }
-    if (tid == 0 && bid < nblk) mbar_wait(&bar[seq & 1], (seq >> 1) & 1);  // drain the prefetch
+    if (tid == 0 && bid < nblk && apend) mbar_wait(&bar[seq & 1], (seq >> 1) & 1);  // drain the prefetch
     if (PROF && a.prof && tid == 0) {  // SM of every CTA (profiling: arrival spread by SM / die)
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -769,7 +771,7 @@ bool cg_persistent_launch_r(const sb_matrix &M, const CgPArgs &proto, bool singl
     static const int bt_env = getenv("SPARSEB200_CG_BT") ? atoi(getenv("SPARSEB200_CG_BT")) : 1;
     const size_t sb_cap = StreamLayout<V, I>(R, cap > 0 ? cap : 64).stage_bytes();
     const bool bt = bt_env && !proto.xa && 5 * (((size_t)R * sizeof(V) + 15) & ~size_t(15)) <= ((sb_cap / 2) & ~size_t(15));
-    auto kern = !single ? (proto.prof ? cg_persistent_kernel<V, I, R, true>
+    auto kern = !single ? (proto.prof ? (bt ? cg_persistent_kernel<V, I, R, true, true> : cg_persistent_kernel<V, I, R, true>)
                            : bt       ? cg_persistent_kernel<V, I, R, false, true>
                                       : cg_persistent_kernel<V, I, R, false>)
                 : mb * R == 768 ? cg1_persistent_kernel<V, I, R, 768 / R> : cg1_persistent_kernel<V, I, R, 1024 / R>;
