@@ -835,7 +835,7 @@ static std::atomic<int> g_cg_mode{[] {
     const char *e = getenv("SPARSEB200_CG_FUSED");
     return e ? atoi(e) : 3;
 }()};
-constexpr size_t kPersistentMaxVectorBytes = 24u << 20;
+constexpr size_t kPersistentMaxVectorBytes = 64u << 20;  // round 2 (staged update phase): 160^3 130.9 vs 134, 192^3 222.9 vs 227.5, 256^3 543 vs 544, 320^3 1080 vs 1041 us per iteration (persistent vs graph)
 // grid barriers per persistent CG iteration: 2 = the two-barrier kernel (default), 1 = the
 // single-sync kernel (SPARSEB200_CG_SYNC=1; measured slower, profiles/README.md round 2)
 static std::atomic<int> g_cg_sync{[] {
@@ -1015,7 +1015,9 @@ sb_status cg_solve(const SolveArgs &a) {
         if (e != cudaSuccess) return e;
         return launch_ew<3>(n, ctl, part, CgInit<V>{{}, b, t, inv, r, z, fused ? nullptr : p}, st);
     };
-    if (mode == 3 && fused && (size_t)n * sizeof(V) <= kPersistentMaxVectorBytes) {
+    static const size_t pmax = getenv("SPARSEB200_CG_PMAX_MB") ? (size_t)atoll(getenv("SPARSEB200_CG_PMAX_MB")) << 20
+                                                                 : kPersistentMaxVectorBytes;
+    if (mode == 3 && fused && (size_t)n * sizeof(V) <= pmax) {
         // one cooperative launch runs every iteration; p ping-pongs between p and t
         h.cond = 0ull;
         SB_CUDA(cudaMemcpyAsync(ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, a.st));
