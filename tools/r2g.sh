@@ -1,5 +1,4 @@
 O=gpurun_out/r2g; mkdir -p $O; rm -f $O/*
-timeout 900 python -m pytest tests/test_gpu_spmv.py tests/test_gpu_formats.py -x -q -p no:cacheprovider > $O/pytest.log 2>&1; echo "rc=$?" >> $O/pytest.log
-timeout 900 python tools/sweep_configs.py --skip-cpu --only 2 > $O/sweep.json 2> $O/sweep.err
-timeout 900 python tools/sweep_configs.py --skip-cpu --only 2 > $O/sweep2.json 2> $O/sweep2.err
+timeout 900 python -m pytest tests/test_gpu_spmv.py -x -q -p no:cacheprovider -m gpu > $O/pytest.log 2>&1; echo "rc=$?" >> $O/pytest.log
+timeout 900 python tools/sweep_configs.py --skip-cpu --only 3 > $O/sweep.json 2> $O/sweep.err
 tail -2 $O/pytest.log
