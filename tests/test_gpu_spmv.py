@@ -341,3 +341,12 @@ def test_sellp_split_pieces(dev, vdt):
         (l0, x0), (l1, x1) = logs
         assert l0.converged and l1.converged and abs(l0.iterations - l1.iterations) <= 1
         np.testing.assert_allclose(x1, x0, rtol=1e-8, atol=1e-10)
+        # the other solvers' loops through the row-splitting operator (no gather epilogues)
+        for cls, kw in ((sp.Gmres, {"krylov_dim": 20}), (sp.Bicgstab, {}), (sp.Cgs, {})):
+            its = []
+            for mat in (spd, sell):
+                x = vec(dev, np.zeros(n))
+                its.append(cls(mat, criteria=crit, preconditioner=sp.jacobi_create(spd), **kw)
+                           .solve(vec(dev, bv), x))
+            assert its[0].converged and its[1].converged, cls
+            assert abs(its[0].iterations - its[1].iterations) <= max(1, its[0].iterations // 50), cls
