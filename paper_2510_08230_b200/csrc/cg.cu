@@ -121,11 +121,41 @@ __device__ __forceinline__ void grid_barrier(unsigned long long *count, unsigned
     __syncthreads();
 }
 
+// The same barrier with CTA-local work in the wait: after arriving, the CTA runs work()
+// steps (each uniform across the CTA; false = nothing left) between polls of the
+// counter, so an early CTA spends the arrival spread on deferred work instead of idling.
+struct NoWork {
+    __device__ __forceinline__ bool operator()() const { return false; }
+};
+template <class W>
+__device__ __forceinline__ void grid_barrier_w(unsigned long long *count, unsigned long long target, W &work) {
+    __shared__ int s_go[2];
+    __syncthreads();
+    if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(count) : "memory");
+    for (unsigned k = 0;; ++k) {
+        if (threadIdx.x == 0) {
+            unsigned long long v;
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(count) : "memory");
+            s_go[k & 1] = v >= target;
+        }
+        __syncthreads();
+        if (s_go[k & 1]) return;  // slot k & 1 is rewritten only after the next __syncthreads
+        if (!work()) break;
+    }
+    if (threadIdx.x == 0) {
+        unsigned long long v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(count) : "memory");
+        } while (v < target);
+    }
+    __syncthreads();
+}
+
 // every CTA publishes its N partials, waits, then sums all G partials in index order
-template <int N, int R>
+template <int N, int R, class W = NoWork>
 __device__ __forceinline__ void grid_allreduce(double (&v)[N], double *partials, unsigned long long *count,
                                                unsigned long long target, double (&tot)[N],
-                                               unsigned long long *stamps = nullptr) {
+                                               unsigned long long *stamps = nullptr, W *work = nullptr) {
     __shared__ double scratch[32][N];
     __shared__ double s_tot[N];
     block_reduce<N>(v, scratch);
@@ -136,7 +166,10 @@ __device__ __forceinline__ void grid_allreduce(double (&v)[N], double *partials,
         if (stamps && target / G >= 10 && target / G < 28)  // arrival stamps of barriers 10..27
             stamps[(target / G - 10) * G + blockIdx.x] = gtimer();
     }
-    grid_barrier(count, target);
+    if constexpr (!std::is_same<W, NoWork>::value)
+        grid_barrier_w(count, target, *work);
+    else
+        grid_barrier(count, target);
     unsigned long long t_rel = 0;
     if (stamps && blockIdx.x == 0 && threadIdx.x == 0) t_rel = gtimer();
     double a[N];
@@ -177,7 +210,13 @@ __host__ __device__ __forceinline__ int64_t cg_block_row(int64_t b, int64_t bq, 
 // instantiation, so the timed kernel carries no timer registers)
 // BT: update-phase operands (q, p_k, x, r, M) TMA-staged two blocks ahead into the stage
 // slot the SpMV ring leaves free during the update (see below)
-template <class V, class I, int R, bool PROF = false, bool BT = false>
+// XW: the x update (x += alpha_k p_k on the own rows, needed by nothing inside the loop)
+// is deferred and run in the grid-barrier waits (grid_barrier_w): it only has to land
+// before p_k's buffer is rewritten two SpMV phases later, and each CTA owns the same
+// rows of x and p in both phases, so the deadline is CTA-local.  What the waits leave
+// over is flushed right after the next alpha (in row order: x_k = x_{k-1} + alpha_k p_k
+// per element, the reference's rounding); the staged update phase reads q, r, M only.
+template <class V, class I, int R, bool PROF = false, bool BT = false, bool XW = false>
 __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar[2];
@@ -226,7 +265,7 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
         unsigned char *dst = smem + (h >> 1) * sb + (h & 1) * hb;
         const int64_t blk = bid + (int64_t)j * G;
         const int64_t r0 = cg_block_row(blk, bq, rem), r1 = min(cg_block_row(blk + 1, bq, rem), n);
-        const V *src[5] = {q, pk, x, r, inv};
+        const V *src[5] = {q, XW ? nullptr : pk, XW ? nullptr : x, r, inv};
         uint32_t by[5], tot = 0;
         int64_t base = r0;
 #pragma unroll
@@ -274,6 +313,32 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
     double alpha = 0.0;
     V *pold = (V *)a.p0, *pnew = (V *)a.p1;
     unsigned long long tp[4] = {0, 0, 0, 0}, t0 = PROF ? gtimer() : 0, t1;
+    // XW: outstanding x update x += xalpha xp on this CTA's blocks xj .. kb-1
+    double xalpha = 0.0;
+    const V *xp = nullptr;
+    int xj = kb;
+    // two blocks per step (four loads in flight per thread; four blocks per step and a
+    // poll issued behind the step's loads measured no better: profiles/README.md)
+    constexpr int XB = 2;
+    auto xstep = [&]() -> bool {
+        if (xj >= kb) return false;
+        int64_t ix[XB];
+        bool ok[XB];
+        V pv[XB], xv[XB];
+#pragma unroll
+        for (int u = 0; u < XB; ++u) {
+            const int64_t bu = bid + (int64_t)(xj + u) * G;
+            ix[u] = cg_block_row(bu, bq, rem) + tid;
+            ok[u] = xj + u < kb && ix[u] < min(cg_block_row(bu + 1, bq, rem), n);
+            pv[u] = ok[u] ? xp[ix[u]] : V(0);
+            xv[u] = ok[u] ? x[ix[u]] : V(0);
+        }
+#pragma unroll
+        for (int u = 0; u < XB; ++u)
+            if (ok[u]) x[ix[u]] = axpy_e(xalpha, pv[u], xv[u]);
+        xj += XB;
+        return true;
+    };
     for (;;) {
         // ---- A: q = A p_k, p_k = z + beta p_{k-1} gathered on the fly
         double part[1] = {0.0};
@@ -334,7 +399,13 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
             bpend = kb < 4 ? kb : 4;
         }
         double pq[1];
-        grid_allreduce<1, R>(part, a.partials, count, ++epoch * G, pq, PROF ? a.prof : nullptr);
+        if constexpr (XW)
+            grid_allreduce<1, R>(part, a.partials, count, ++epoch * G, pq, PROF ? a.prof : nullptr, &xstep);
+        else
+            grid_allreduce<1, R>(part, a.partials, count, ++epoch * G, pq, PROF ? a.prof : nullptr);
+        if constexpr (XW)
+            while (xstep()) {
+            }  // the rest of x_{k-1} += alpha_{k-1} p_{k-1} before p_{k+1} reuses that buffer
         if constexpr (PROF) {
             t1 = gtimer();
             tp[1] += t1 - t0;
@@ -349,6 +420,11 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
             break;
         }
         alpha = rz / pq[0];
+        if constexpr (XW) {
+            xalpha = alpha;
+            xp = pnew;
+            xj = 0;
+        }
         // ---- B: x += alpha p_k; r -= alpha q; z = M r; r.r, r.z on the rows of this CTA's
         // own SpMV blocks (same moving window over memory as phase A; measured faster than
         // a balanced contiguous split, which scatters the accesses over the whole vectors)
@@ -364,7 +440,7 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
                 const int64_t blk = bid + (int64_t)j * G;
                 const int64_t i = cg_block_row(blk, bq, rem) + tid;  // block rows start 32-aligned: slot index tid
                 if (i < min(cg_block_row(blk + 1, bq, rem), n)) {
-                    x[i] = axpy_e(alpha, sp[tid], sx[tid]);
+                    if constexpr (!XW) x[i] = axpy_e(alpha, sp[tid], sx[tid]);
                     const V ri = axpy_e(-alpha, sq[tid], sr[tid]);
                     const V zi = inv ? vmul(ri, sd[tid]) : ri;
                     r[i] = ri;
@@ -410,7 +486,10 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
             t0 = t1;
         }
         double tot[2];
-        grid_allreduce<2, R>(part2, a.partials + G, count, ++epoch * G, tot, PROF ? a.prof : nullptr);
+        if constexpr (XW)
+            grid_allreduce<2, R>(part2, a.partials + G, count, ++epoch * G, tot, PROF ? a.prof : nullptr, &xstep);
+        else
+            grid_allreduce<2, R>(part2, a.partials + G, count, ++epoch * G, tot, PROF ? a.prof : nullptr);
         if constexpr (PROF) {
             t1 = gtimer();
             tp[3] += t1 - t0;
@@ -440,6 +519,9 @@ __global__ void __launch_bounds__(R, 1024 / R) cg_persistent_kernel(CgPArgs a) {
         pold = pnew;
         pnew = t;
     }
+    if constexpr (XW)
+        while (xstep()) {
+        }  // the outstanding x update (every exit: x holds the last accepted iterate)
     if (flush)  // the last iteration's x update (x_k = x_{k-1} + alpha_k p_k, own rows)
         for (int j = 0; j < kb; ++j) {
             const int64_t blk = bid + (int64_t)j * G;
@@ -771,9 +853,16 @@ bool cg_persistent_launch_r(const sb_matrix &M, const CgPArgs &proto, bool singl
     static const int bt_env = getenv("SPARSEB200_CG_BT") ? atoi(getenv("SPARSEB200_CG_BT")) : 1;
     const size_t sb_cap = StreamLayout<V, I>(R, cap > 0 ? cap : 64).stage_bytes();
     const bool bt = bt_env && !proto.xa && 5 * (((size_t)R * sizeof(V) + 15) & ~size_t(15)) <= ((sb_cap / 2) & ~size_t(15));
-    auto kern = !single ? (proto.prof ? (bt ? cg_persistent_kernel<V, I, R, true, true> : cg_persistent_kernel<V, I, R, true>)
-                           : bt       ? cg_persistent_kernel<V, I, R, false, true>
-                                      : cg_persistent_kernel<V, I, R, false>)
+    // x update in the barrier waits (staged update phase only; SPARSEB200_CG_XW=0 turns it
+    // off: 128^3 68.4-68.9 -> 66.3-66.9 us per iteration, same box)
+    static const int xw_env = getenv("SPARSEB200_CG_XW") ? atoi(getenv("SPARSEB200_CG_XW")) : 1;
+    const bool xw = bt && xw_env;
+    auto kern = !single ? (proto.prof ? (xw ? cg_persistent_kernel<V, I, R, true, true, true>
+                                        : bt ? cg_persistent_kernel<V, I, R, true, true>
+                                             : cg_persistent_kernel<V, I, R, true>)
+                           : xw ? cg_persistent_kernel<V, I, R, false, true, true>
+                           : bt ? cg_persistent_kernel<V, I, R, false, true>
+                                : cg_persistent_kernel<V, I, R, false>)
                 : mb * R == 768 ? cg1_persistent_kernel<V, I, R, 768 / R> : cg1_persistent_kernel<V, I, R, 1024 / R>;
     ensure_max_smem((const void *)kern);
     int occ = 0;

@@ -13,7 +13,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
    --log-file $O/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu > $O/ncu_bench.log 2>&1
 timeout 600 ncu --set full --clock-control none -k regex:cg_persistent -s 1 -c 1 -o $O/cg python tools/cg_ab.py 128 > $O/ncu_cg.log 2>&1
 timeout 600 ncu --set full --clock-control none -k regex:csr_stream_kernel -s 3 -c 1 -o $O/spmv python tools/prof_cg.py 128 > $O/ncu_spmv.log 2>&1
-timeout 1500 python tools/sweep_configs.py --skip-cpu > $O/sweep.json 2> $O/sweep.err
+[ -z "$SKIP_SWEEP" ] && timeout 1500 python tools/sweep_configs.py --skip-cpu > $O/sweep.json 2> $O/sweep.err
 tail -2 $O/pytest_gpu.log; cat $O/smoke.log | tail -1; cut -c1-300 $O/bench.json
 # post-process the --set full reports on the box (the .ncu-rep files exceed the 64 MiB copy-back)
 for r in cg spmv; do
