@@ -1124,13 +1124,49 @@ __device__ __forceinline__ void padded_rows(const Epi &epi, const V *__restrict_
             for (int r = 0; r < RPT; ++r)
                 if (cc[u][r] >= 0) acc[r] = addd(acc[r], mulp(vv[u][r], gg[u][r]));
     }
-    for (; k < len; ++k) {
-        V vv[RPT];
-        I cc[RPT];
-        load_column<V, I, RPT>(val, col, base0 + k * kstride, vv, cc);
+    if (sizeof(V) == 4) {  // fp32 (four rows per thread): the one-column loop measured faster
+        for (; k < len; ++k) {
+            V vv[RPT];
+            I cc[RPT];
+            load_column<V, I, RPT>(val, col, base0 + k * kstride, vv, cc);
 #pragma unroll
-        for (int r = 0; r < RPT; ++r)
-            if (cc[r] >= 0) acc[r] = addd(acc[r], mulp(vv[r], gather_b(epi, b, bidx<U1>((int64_t)cc[r], ldb))));
+            for (int r = 0; r < RPT; ++r)
+                if (cc[r] >= 0) acc[r] = addd(acc[r], mulp(vv[r], gather_b(epi, b, bidx<U1>((int64_t)cc[r], ldb))));
+        }
+    } else if (k < len) {
+        // the last 1-3 columns as one more four-column step (columns past len skipped by a
+        // uniform predicate, their indices set to padding): every load and gather of the
+        // tail is in flight before the first add, instead of one dependent load -> gather
+        // -> add round per column (128^3 has 7 columns = 4 + 3: fp64 ELL 37.8 -> 34.2 us,
+        // Hybrid 37.9 -> 34.0; fp32 measured slower with it, 29.6 -> 30.1)
+        V vv[4][RPT], gg[4][RPT];
+        I cc[4][RPT];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (k + u < len) {
+                load_column<V, I, RPT>(val, col, base0 + (k + u) * kstride, vv[u], cc[u]);
+            } else {
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) {
+                    vv[u][r] = V(0);
+                    cc[u][r] = (I)-1;
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                if constexpr (epi_has_gather<Epi>::value)
+                    gg[u][r] = gather_b(epi, b, bidx<U1>((int64_t)(cc[u][r] >= 0 ? cc[u][r] : 0), ldb));
+                else
+                    gg[u][r] = cc[u][r] >= 0 ? __ldg(b + bidx<U1>((int64_t)cc[u][r], ldb)) : (V)0;
+            }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int r = 0; r < RPT; ++r)
+                if (cc[u][r] >= 0) acc[r] = addd(acc[r], mulp(vv[u][r], gg[u][r]));
     }
 }
 
@@ -1299,9 +1335,18 @@ __global__ void __launch_bounds__(128) sellp_block_kernel(int64_t rows, int64_t 
                 I cc[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {  // branch-free tail (see csr_stream_kernel)
-                    const int e = (k + u < len ? k + u : len - 1) * S;
-                    vv[u] = sv[ov + e];
-                    cc[u] = k + u < len ? sc[oc + e] : (I)-1;
+                    const bool on = k + u < len;
+                    if constexpr (sizeof(V) == 4) {
+                        // fp32: predicated stage reads at fixed offsets from one base (no
+                        // clamped index; 128^3 SELL-P(64) 29.5 -> 26.4 us; fp64 measured
+                        // slower with it, 34.7 -> 35.5, and keeps the clamped index)
+                        vv[u] = on ? sv[ov + (k + u) * S] : V(0);
+                        cc[u] = on ? sc[oc + (k + u) * S] : (I)-1;
+                    } else {
+                        const int e = (on ? k + u : len - 1) * S;
+                        vv[u] = sv[ov + e];
+                        cc[u] = on ? sc[oc + e] : (I)-1;
+                    }
                     bb[u] = gather_b(epi, b, bidx<U1>((int64_t)(cc[u] >= 0 ? cc[u] : 0), ldb));
                 }
 #pragma unroll
@@ -1434,9 +1479,15 @@ __global__ void __launch_bounds__(128) sellp_chunk_kernel(int64_t rows, int64_t 
                 I cc[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {  // branch-free tail (see csr_stream_kernel)
-                    const int kk = k + u < kend ? k + u : kend - 1;
-                    vv[u] = sv[ov + (int64_t)kk * S];
-                    cc[u] = k + u < kend ? sc[oc + (int64_t)kk * S] : (I)-1;
+                    const bool on = k + u < kend;
+                    if constexpr (sizeof(V) == 4) {  // fp32: predicated reads at fixed offsets
+                        vv[u] = on ? sv[ov + (int64_t)(k + u) * S] : V(0);
+                        cc[u] = on ? sc[oc + (int64_t)(k + u) * S] : (I)-1;
+                    } else {
+                        const int kk = on ? k + u : kend - 1;
+                        vv[u] = sv[ov + (int64_t)kk * S];
+                        cc[u] = on ? sc[oc + (int64_t)kk * S] : (I)-1;
+                    }
                     if constexpr (epi_has_gather<Epi>::value)  // padding: col 0, masked below
                         bb[u] = gather_b(epi, b, bidx<U1>((int64_t)(cc[u] >= 0 ? cc[u] : 0), ldb));
                     else
