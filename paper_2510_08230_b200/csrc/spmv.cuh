@@ -1080,6 +1080,9 @@ __device__ __forceinline__ void load_column(const V *__restrict__ val, const I *
     if constexpr (RPT * sizeof(V) == 16) {
         int4 raw = __ldcs(reinterpret_cast<const int4 *>(val + base));
         memcpy(vv, &raw, 16);
+    } else if constexpr (RPT * sizeof(V) == 8) {
+        int2 raw = __ldcs(reinterpret_cast<const int2 *>(val + base));
+        memcpy(vv, &raw, 8);
     } else {
 #pragma unroll
         for (int r = 0; r < RPT; ++r) vv[r] = __ldcs(val + base + r);
@@ -1124,7 +1127,7 @@ __device__ __forceinline__ void padded_rows(const Epi &epi, const V *__restrict_
             for (int r = 0; r < RPT; ++r)
                 if (cc[u][r] >= 0) acc[r] = addd(acc[r], mulp(vv[u][r], gg[u][r]));
     }
-    if (sizeof(V) == 4) {  // fp32 (four rows per thread): the one-column loop measured faster
+    if (RPT * sizeof(V) == 16 && sizeof(V) == 4) {  // fp32, four rows per thread: the one-column loop measured faster
         for (; k < len; ++k) {
             V vv[RPT];
             I cc[RPT];
