@@ -220,6 +220,11 @@ void sb_set_cg_fused(int mode);
    steps, beta within a few ulps; measured slower on B200, kept opt-in).  Replaces nothing
    in the reference (solvers.py:188-224 is one loop shape). */
 void sb_set_cg_sync(int barriers);
+/* Persistent CG (two-barrier kernel): 1 (default) = the x update x += alpha p runs inside
+   the grid-barrier waits and is flushed before its p buffer is reused (bitwise the same
+   x); 0 = x updated in the update phase.  Replaces nothing in the reference
+   (solvers.py:200-224 updates x in place each iteration; the element arithmetic is that). */
+void sb_set_cg_xw(int on);
 /* Loop shape used by this thread's last CG solve: 0 three-kernel graph loop, 1 fused-
    direction graph loop, 3 persistent cooperative kernel (one launch per solve). */
 int sb_cg_last_loop(void);

@@ -193,6 +193,7 @@ _PLAIN_PROTOS = {
     "sb_set_graph_mode": (None, [c_i32]),
     "sb_set_cg_fused": (None, [c_i32]),
     "sb_set_cg_sync": (None, [c_i32]),
+    "sb_set_cg_xw": (None, [c_i32]),
     "sb_cg_last_loop": (c_i32, []),
     "sb_cg_last_block_rows": (c_i32, []),
     "sb_tri_workspace_bytes": (c_sz, [c_i64]),

@@ -809,6 +809,11 @@ __global__ void cg_block_nnz_max_kernel(const I *rp, int64_t n, int64_t nblk, in
 // balanced blocks (<= R rows each, whole 32-row units), so every CTA owns exactly kb blocks.
 static thread_local int g_cg_last_rows = 0;  // block rows of the last persistent launch
 
+static std::atomic<int> g_cg_xw{[] {
+    const char *e = getenv("SPARSEB200_CG_XW");
+    return e ? atoi(e) : 1;
+}()};
+
 template <class V, class I, int R>
 bool cg_persistent_launch_r(const sb_matrix &M, const CgPArgs &proto, bool single, cudaStream_t st, cudaError_t &err) {
     err = cudaSuccess;
@@ -853,10 +858,9 @@ bool cg_persistent_launch_r(const sb_matrix &M, const CgPArgs &proto, bool singl
     static const int bt_env = getenv("SPARSEB200_CG_BT") ? atoi(getenv("SPARSEB200_CG_BT")) : 1;
     const size_t sb_cap = StreamLayout<V, I>(R, cap > 0 ? cap : 64).stage_bytes();
     const bool bt = bt_env && !proto.xa && 5 * (((size_t)R * sizeof(V) + 15) & ~size_t(15)) <= ((sb_cap / 2) & ~size_t(15));
-    // x update in the barrier waits (staged update phase only; SPARSEB200_CG_XW=0 turns it
-    // off: 128^3 68.4-68.9 -> 66.3-66.9 us per iteration, same box)
-    static const int xw_env = getenv("SPARSEB200_CG_XW") ? atoi(getenv("SPARSEB200_CG_XW")) : 1;
-    const bool xw = bt && xw_env;
+    // x update in the barrier waits (staged update phase only; sb_set_cg_xw(0) /
+    // SPARSEB200_CG_XW=0 turns it off: 128^3 68.4-68.9 -> 66.3-66.9 us per iteration)
+    const bool xw = bt && g_cg_xw.load() != 0;
     auto kern = !single ? (proto.prof ? (xw ? cg_persistent_kernel<V, I, R, true, true, true>
                                         : bt ? cg_persistent_kernel<V, I, R, true, true>
                                              : cg_persistent_kernel<V, I, R, true>)
@@ -1216,6 +1220,7 @@ extern "C" {
 
 void sb_set_cg_fused(int mode) { g_cg_mode = mode; }
 void sb_set_cg_sync(int barriers) { g_cg_sync = barriers == 1 ? 1 : 2; }
+void sb_set_cg_xw(int on) { g_cg_xw = on ? 1 : 0; }
 int sb_cg_last_loop(void) { return g_cg_last_loop; }
 int sb_cg_last_block_rows(void) { return g_cg_last_loop == 3 ? g_cg_last_rows : 0; }
 

@@ -307,6 +307,36 @@ def test_cg_persistent_kernel(dev, dtype):
         set_mode(3)
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_cg_persistent_x_update_in_barrier_waits(dev, dtype):
+    """The persistent CG's x update deferred into the grid-barrier waits (sb_set_cg_xw(1),
+    the default) changes only WHEN x += alpha p runs, not its per-element order or
+    rounding: x and the residual history are bitwise those of the in-phase update, for
+    converged, odd / even max_iters, x0 != 0 and breakdown exits."""
+    from paper_2510_08230_b200 import _lib
+    prec = sp.Precision.from_dtype(np.dtype(dtype))
+    a = gen.stencil_csr(dev, 40, dim=3, precision=prec)
+    rng = np.random.default_rng(11)
+    b = rng.random(a.rows).astype(dtype)
+    x0 = rng.random(a.rows).astype(dtype)
+    set_xw = _lib.fn("sb_set_cg_xw")
+    try:
+        for crit, xi in (([sp.Iteration(5000), sp.ResidualNorm(1e-7)], None),
+                         ([sp.Iteration(7)], x0), ([sp.Iteration(8)], x0),
+                         ([sp.Iteration(5000), sp.ResidualNorm(1e-6)], x0)):
+            out = {}
+            for xw in (0, 1):
+                set_xw(xw)
+                out[xw] = solve(dev, "cg", a, b, crit, x0=xi)
+                assert _lib.fn("sb_cg_last_loop")() == 3
+            (l0, x0r, _), (l1, x1r, _) = out[0], out[1]
+            assert l0.iterations == l1.iterations and l0.stop_reason == l1.stop_reason
+            np.testing.assert_array_equal(np.asarray(l1.residual_history), np.asarray(l0.residual_history))
+            np.testing.assert_array_equal(x1r, x0r)
+    finally:
+        set_xw(1)
+
+
 @pytest.mark.parametrize("kind", ["cg", "cgs", "bicgstab", "gmres"])
 def test_graph_cache_tracks_workspace_layout(dev, kind):
     """A captured solver loop is reused only for the same buffers: the workspace's vector
